@@ -1,0 +1,146 @@
+/*
+ * nwb200 -- C ABI of the B200 ExpRK22/WENO5 step (libnwb200.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference `nwave`
+ * package (arXiv 2103.06080).  The reference binds no FFI of its own (its
+ * path is Python + numba + scipy.fft); each entry point below replaces one
+ * reference function, cited as file:line under /root/reference/pkg/src/nwave:
+ *
+ *   nwb_plan_create / nwb_plan_set_coeffs / nwb_plan_load_* / nwb_march /
+ *   nwb_plan_store_physical             -> run_exprk22      exprk.py:219-331
+ *   nwb_step (scheme)                   -> exprk22_step     exprk.py:151-178
+ *                                          exp_euler_step   exprk.py:181-196
+ *   nwb_rfft2 / nwb_irfft2              -> SpectralTransforms.forward/inverse
+ *                                                           exprk.py:134-148
+ *   nwb_tables                          -> build_multipliers exprk.py:111-131
+ *   nwb_phi                             -> phi1 / phi2      exprk.py:42-84
+ *   nwb_combine                         -> the numpy combines of exprk.py:166-173,193
+ *   nwb_weno5_b                         -> weno5_b          weno.py:106-124
+ *
+ * Conventions.  Plain pointers and sizes only.  Buffer arguments named *_dev
+ * are device pointers (the Python layer passes torch CUDA tensors'
+ * data_ptr()); everything else is host memory.  Real arrays are float64 for
+ * NWB_F64 plans and float32 for NWB_F32; complex arrays are interleaved
+ * (re, im) pairs of the same real type.  Physical fields are
+ * (batch, n_rho, n_theta) row-major; spectra handed across the boundary
+ * are (batch, n_rho, n_theta/2 + 1) row-major in numpy.fft order, exactly
+ * scipy's rfft2 layout.  A plan is bound to one device and one stream and is
+ * not re-entrant; plans on different devices may be driven from different
+ * host threads.
+ *
+ * Return codes: 0 on success, negative NWB_E* on failure; the message is
+ * available from nwb_last_error() (thread-local).  The Python layer maps
+ * NWB_EINVAL -> ValueError, NWB_EUNSUPPORTED -> UnsupportedSizeError,
+ * NWB_EINSTABILITY -> InstabilityError, NWB_EBUDGET -> BudgetExceededError,
+ * NWB_ECUDA / NWB_ENOMEM -> BackendError.
+ */
+#ifndef NWB200_H
+#define NWB200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NWB_OK 0
+#define NWB_EINVAL (-1)
+#define NWB_EUNSUPPORTED (-2)
+#define NWB_ECUDA (-3)
+#define NWB_ENOMEM (-4)
+#define NWB_EINSTABILITY (-5)
+#define NWB_EBUDGET (-6)
+
+#define NWB_F64 0
+#define NWB_F32 1
+
+#define NWB_SCHEME_EXPRK22 0
+#define NWB_SCHEME_EXPEULER 1
+
+typedef struct nwb_plan nwb_plan;
+
+int nwb_abi_version(void);
+const char* nwb_last_error(void);
+int nwb_device_count(void);
+
+/* Plan: device tables (E, Phi1, Phi2, Phi1-Phi2 in digit-reversed rho order),
+ * FFT twiddles, coefficient rows and all step workspaces for `batch`
+ * independent members sharing one grid.  eps is the working-precision
+ * machine epsilon used by the regularised multiplier (exprk.py:114-116).
+ * Returns NWB_EUNSUPPORTED when n_rho or n_theta/2 has a prime factor above
+ * 7, n_theta is odd, or a transform does not fit in shared memory. */
+int nwb_plan_create(nwb_plan** plan, int n_rho, int n_theta, int batch, int precision,
+                    double d_sigma, double rho_span, double theta_span, double A, double B,
+                    double eps, int device);
+int nwb_plan_destroy(nwb_plan* plan);
+int nwb_plan_set_stream(nwb_plan* plan, void* stream);
+/* Workspace footprint in bytes (device). */
+long long nwb_plan_bytes(const nwb_plan* plan);
+
+/* Coefficient rows U_par, U_perp, dU_perp/drho for sigma rows 0..n_rows-1,
+ * row r at base + r*ld (ld >= n_rho; extra columns ignored, exprk.py:261-263).
+ * Host float64 when on_device == 0, device float64 when 1.  They are cast to
+ * the working precision and stay resident; alpha_rho per row is precomputed.
+ * NULL pointers mean a quiescent medium (U = 0). */
+int nwb_plan_set_coeffs(nwb_plan* plan, const double* u_par, const double* u_perp,
+                        const double* du_drho, int n_rows, int ld, int on_device);
+
+/* State in: physical V0 (batch, n_rho, n_theta) working precision, device. */
+int nwb_plan_load_physical(nwb_plan* plan, const void* v0_dev);
+/* State in/out: natural-order half spectrum (batch, n_rho, n_theta/2+1), device. */
+int nwb_plan_load_spectrum(nwb_plan* plan, const void* vhat_dev);
+int nwb_plan_store_spectrum(nwb_plan* plan, void* vhat_dev);
+/* State out: V = irfft2(Vhat) (batch, n_rho, n_theta), device; max|V| per
+ * member into max_abs_host (may be NULL). */
+int nwb_plan_store_physical(nwb_plan* plan, void* v_dev, double* max_abs_host);
+
+/* March n_steps steps from absolute step n0 (coefficient rows n0..n0+n_steps).
+ *   snap_steps[i] / snap_bufs_dev[i]: copy V_n (the field at the start of
+ *     step n, exprk.py:301-302) for the listed absolute steps into the given
+ *     device buffers (batch, n_rho, n_theta).
+ *   max_abs_host: [batch * n_steps] max|V_n| per member and step (or NULL).
+ *   step_ms_host: [n_steps * 3] = (step, nonlinear, linear) device ms from
+ *     CUDA events, or NULL (then steps are replayed from a CUDA graph).
+ *   guard: stop with NWB_EINSTABILITY at the first step whose max|V_n| is
+ *     non-finite or > guard; *fail_step, *fail_member, *fail_value say where.
+ *   max_seconds > 0: stop with NWB_EBUDGET once the host wall clock exceeds it
+ *     (checked at synchronisation points); *fail_step = steps completed. */
+int nwb_march(nwb_plan* plan, int scheme, int n0, int n_steps, double guard,
+              double max_seconds, const int* snap_steps, int n_snap,
+              void* const* snap_bufs_dev, double* max_abs_host, float* step_ms_host,
+              int* fail_step, int* fail_member, double* fail_value);
+
+/* One step from absolute step n without guard bookkeeping (graph-free). */
+int nwb_step(nwb_plan* plan, int scheme, int n);
+
+/* SpectralTransforms: rfft2 (batch, n_rho, n_theta) real -> natural half
+ * spectrum; irfft2 the inverse (Im of the theta DC / Nyquist bins dropped,
+ * scaled 1/(n_rho n_theta)). */
+int nwb_rfft2(nwb_plan* plan, const void* in_dev, void* out_dev);
+int nwb_irfft2(nwb_plan* plan, const void* in_dev, void* out_dev);
+
+/* weno5_b on (batch, n_rho, n_theta) (no plan, any extents): coefficient
+ * vectors are length-n_rho device arrays in the working precision (shared by
+ * all members); workspace_dev holds >= 8*(batch+1) bytes. */
+int nwb_weno5_b(int precision, int batch, int n_rho, int n_theta, const void* v_dev,
+                const void* u_par_dev, const void* u_perp_dev, const void* du_dev,
+                double b_coef, double d_rho, double d_theta, void* out_dev,
+                void* workspace_dev, void* stream);
+
+/* Standalone multiplier tables in natural (n_rho, n_theta/2+1) layout; any
+ * output may be NULL.  z is always complex128. */
+int nwb_tables(int precision, int n_rho, int n_theta, double rho_span, double theta_span,
+               double d_sigma, double A, double eps, void* E_dev, void* P1_dev, void* P2_dev,
+               void* P12_dev, void* z_dev, void* stream);
+/* phi_shift(z) for complex128 z (shift 1 or 2). */
+int nwb_phi(const void* z_dev, long long n, int shift, void* out_dev, void* stream);
+/* Elementwise combines with numpy rounding (no FMA):
+ * mode 0: out = E*vh; 1: out = vh + (ds*P1)*b1; 2: out = vh + ds*(P12*b1 + P2*b2);
+ * 3: out = E*vh + (ds*P1)*b1. */
+int nwb_combine(int precision, long long n, int mode, double d_sigma, const void* E_dev,
+                const void* P1_dev, const void* P12_dev, const void* P2_dev,
+                const void* vh_dev, const void* b1_dev, const void* b2_dev, void* out_dev,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

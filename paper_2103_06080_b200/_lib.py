@@ -1,0 +1,135 @@
+"""ctypes binding of libnwb200.so (the C ABI in include/nwb200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every entry point raises ``BackendError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import (BackendError, BudgetExceededError, InstabilityError,
+                     UnsupportedSizeError)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnwb200.so")
+
+NWB_OK = 0
+NWB_EINVAL = -1
+NWB_EUNSUPPORTED = -2
+NWB_ECUDA = -3
+NWB_ENOMEM = -4
+NWB_EINSTABILITY = -5
+NWB_EBUDGET = -6
+
+F64 = 0
+F32 = 1
+SCHEME_EXPRK22 = 0
+SCHEME_EXPEULER = 1
+
+ABI_SYMBOLS = (
+    "nwb_abi_version", "nwb_last_error", "nwb_device_count", "nwb_plan_create",
+    "nwb_plan_destroy", "nwb_plan_set_stream", "nwb_plan_bytes", "nwb_plan_set_coeffs",
+    "nwb_plan_load_physical", "nwb_plan_load_spectrum", "nwb_plan_store_spectrum",
+    "nwb_plan_store_physical", "nwb_march", "nwb_step", "nwb_rfft2", "nwb_irfft2",
+    "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine",
+)
+
+_lock = threading.Lock()
+_lib = None
+
+c_int, c_double, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+c_ll = ctypes.c_longlong
+P = ctypes.POINTER
+
+
+def _declare(lib):
+    sig = {
+        "nwb_abi_version": (c_int, []),
+        "nwb_last_error": (ctypes.c_char_p, []),
+        "nwb_device_count": (c_int, []),
+        "nwb_plan_create": (c_int, [P(c_void_p), c_int, c_int, c_int, c_int, c_double,
+                                    c_double, c_double, c_double, c_double, c_double, c_int]),
+        "nwb_plan_destroy": (c_int, [c_void_p]),
+        "nwb_plan_set_stream": (c_int, [c_void_p, c_void_p]),
+        "nwb_plan_bytes": (c_ll, [c_void_p]),
+        "nwb_plan_set_coeffs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                        c_int]),
+        "nwb_plan_load_physical": (c_int, [c_void_p, c_void_p]),
+        "nwb_plan_load_spectrum": (c_int, [c_void_p, c_void_p]),
+        "nwb_plan_store_spectrum": (c_int, [c_void_p, c_void_p]),
+        "nwb_plan_store_physical": (c_int, [c_void_p, c_void_p, c_void_p]),
+        "nwb_march": (c_int, [c_void_p, c_int, c_int, c_int, c_double, c_double, c_void_p,
+                              c_int, c_void_p, c_void_p, c_void_p, P(c_int), P(c_int),
+                              P(c_double)]),
+        "nwb_step": (c_int, [c_void_p, c_int, c_int]),
+        "nwb_rfft2": (c_int, [c_void_p, c_void_p, c_void_p]),
+        "nwb_irfft2": (c_int, [c_void_p, c_void_p, c_void_p]),
+        "nwb_weno5_b": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_double, c_double, c_double, c_void_p, c_void_p,
+                                c_void_p]),
+        "nwb_tables": (c_int, [c_int, c_int, c_int, c_double, c_double, c_double, c_double,
+                               c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p]),
+        "nwb_phi": (c_int, [c_void_p, c_ll, c_int, c_void_p, c_void_p]),
+        "nwb_combine": (c_int, [c_int, c_ll, c_int, c_double, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+
+
+def load_library():
+    """Load libnwb200.so (no device needed); raises BackendError if absent."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise BackendError(
+                    f"{LIB_PATH} is missing: build it with `python -m "
+                    "paper_2103_06080_b200._build` (there is no CPU fallback)")
+            try:
+                lib = ctypes.CDLL(LIB_PATH)
+            except OSError as exc:  # pragma: no cover - loader failure
+                raise BackendError(f"cannot load {LIB_PATH}: {exc}") from exc
+            _declare(lib)
+            _lib = lib
+    return _lib
+
+
+def lib():
+    """The library, after checking that a CUDA device is usable."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise BackendError("no CUDA device visible: the B200 backend has no CPU fallback")
+    return load_library()
+
+
+def last_error() -> str:
+    raw = load_library().nwb_last_error()
+    return raw.decode(errors="replace") if raw else ""
+
+
+def check(rc: int, what: str = ""):
+    if rc == NWB_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == NWB_EINVAL:
+        raise ValueError(msg)
+    if rc == NWB_EUNSUPPORTED:
+        raise UnsupportedSizeError(msg)
+    if rc == NWB_EINSTABILITY:
+        raise InstabilityError(float("nan"), float("nan"))
+    if rc == NWB_EBUDGET:
+        raise BudgetExceededError(msg)
+    raise BackendError(f"{msg} (code {rc})")
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (or None)."""
+    return None if t is None else t.data_ptr()

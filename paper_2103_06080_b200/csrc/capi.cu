@@ -1,0 +1,859 @@
+// C ABI and native runtime of the B200 ExpRK22/WENO5 step: plans (device
+// tables, twiddles, workspaces), the sigma-march driver (CUDA graphs or
+// per-step events, guard and budget checks, snapshots) and the standalone
+// entry points that back the Python drop-in API.  See include/nwb200.h.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nwb200.h"
+#include "internal.h"
+
+using namespace nwb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(e_ == cudaErrorMemoryAllocation ? NWB_ENOMEM : NWB_ECUDA,            \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+  } while (0)
+
+#define CHECK_LAUNCH(what)                                                             \
+  do {                                                                                 \
+    cudaError_t e_ = cudaGetLastError();                                               \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(NWB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+// radices for an n-point complex transform: 7s, 5s, 3s, then 8s and a 4 / 2
+bool factorize(int n, FftDesc& d) {
+  std::vector<int> r;
+  int m = n, twos = 0;
+  while (m % 2 == 0) { m /= 2; ++twos; }
+  for (int p : {7, 5, 3})
+    while (m % p == 0) { m /= p; r.push_back(p); }
+  if (m != 1) return false;
+  while (twos >= 3) { r.push_back(8); twos -= 3; }
+  if (twos == 2) r.push_back(4);
+  if (twos == 1) r.push_back(2);
+  if ((int)r.size() > NWB_MAX_STAGES) return false;
+  d.n = n;
+  d.nst = (int)r.size();
+  int L = n;
+  for (int i = 0; i < d.nst; ++i) {
+    d.radix[i] = r[i];
+    d.span[i] = L;
+    L /= r[i];
+  }
+  return true;
+}
+
+// position after a DIF pass -> frequency
+std::vector<int> freq_of_pos(const FftDesc& d) {
+  std::vector<int> f(d.n);
+  for (int p = 0; p < d.n; ++p) {
+    int rem = p, ff = 0, mult = 1;
+    for (int s = 0; s < d.nst; ++s) {
+      const int span = d.span[s] / d.radix[s];
+      const int q = rem / span;
+      rem -= q * span;
+      ff += q * mult;
+      mult *= d.radix[s];
+    }
+    f[p] = ff;
+  }
+  return f;
+}
+
+// W_n^t = exp(-2 pi i t / n) in extended precision, t < count
+template <typename T> std::vector<cplx<T>> twiddles(int n, int count) {
+  std::vector<cplx<T>> w(count);
+  const long double pi = 3.141592653589793238462643383279502884L;
+  for (int t = 0; t < count; ++t) {
+    // reduce to the first octant for accuracy: angle = 2 pi t / n
+    const long double a = 2.0L * pi * (long double)t / (long double)n;
+    w[t].x = (T)cosl(a);
+    w[t].y = (T)-sinl(a);
+  }
+  return w;
+}
+
+}  // namespace
+
+struct nwb_plan {
+  int device = 0;
+  cudaStream_t stream = 0;
+  cudaStream_t own_stream = 0;  // used when the caller sets none (graphs cannot capture the legacy stream)
+  int prec = NWB_F64;
+  Geom g{};
+  double d_sigma = 0, rho_span = 0, theta_span = 0, A = 0, B = 0, eps = 0;
+  FftDesc dr{}, dh{};
+  int theta_rows = 1, rho_threads = 256;
+  size_t rsz = 8;  // sizeof(real)
+  // device buffers
+  void *tw_r = nullptr, *tw_h = nullptr, *wk = nullptr;
+  int *pos_r = nullptr, *rev_r = nullptr, *pos_h = nullptr;
+  void *vh = nullptr, *u = nullptr, *t = nullptr, *ts = nullptr, *bt = nullptr;
+  void *v = nullptr, *b = nullptr;
+  void *E = nullptr, *P1 = nullptr, *P12 = nullptr, *P2 = nullptr;
+  void *upar = nullptr, *uperp = nullptr, *du = nullptr;
+  double* alpha_rho = nullptr;
+  int n_rows = 0;
+  u64* red = nullptr;        // [batch][4]: alpha stage 1, alpha stage 2, scratch, scratch
+  u64* vmax_hist = nullptr;  // [batch][hist_len]
+  int hist_len = 0;
+  int* step_ctr = nullptr;
+  long long bytes = 0;
+  // graphs (one captured step per scheme)
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  cudaStream_t graph_stream[2] = {nullptr, nullptr};
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int dalloc(nwb_plan* p, void** ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? NWB_ENOMEM : NWB_ECUDA,
+                std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  p->allocs.push_back(*ptr);
+  p->bytes += (long long)bytes;
+  return NWB_OK;
+}
+
+#define TRY(x)                 \
+  do {                         \
+    int rc_ = (x);             \
+    if (rc_ != NWB_OK) return rc_; \
+  } while (0)
+
+template <typename T> ThetaArgs<T> theta_args(const nwb_plan* p) {
+  ThetaArgs<T> a{};
+  a.g = p->g;
+  a.dh = p->dh;
+  a.tw_h = (const cplx<T>*)p->tw_h;
+  a.wk = (const cplx<T>*)p->wk;
+  a.pos_h = p->pos_h;
+  a.scale = (T)(1.0 / ((double)p->g.nr * (double)p->g.nt));
+  a.bcoef = (T)p->B;
+  a.alpha_stride = 4;
+  a.vmax_stride = p->hist_len;
+  return a;
+}
+
+template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
+  RhoArgs<T> a{};
+  a.g = p->g;
+  a.dr = p->dr;
+  a.tw_r = (const cplx<T>*)p->tw_r;
+  a.pos_r = p->pos_r;
+  a.vh = (cplx<T>*)p->vh;
+  a.u = (cplx<T>*)p->u;
+  a.E = (const cplx<T>*)p->E;
+  a.P1 = (const cplx<T>*)p->P1;
+  a.P12 = (const cplx<T>*)p->P12;
+  a.P2 = (const cplx<T>*)p->P2;
+  a.ds = (T)p->d_sigma;
+  a.zero_stride = 4;
+  return a;
+}
+
+template <typename T> WenoArgs<T> weno_args(const nwb_plan* p) {
+  WenoArgs<T> a{};
+  a.g = p->g;
+  a.v = (const T*)p->v;
+  a.out = (T*)p->b;
+  a.upar = (const T*)p->upar;
+  a.uperp = (const T*)p->uperp;
+  a.du = (const T*)p->du;
+  a.alpha_rho = p->alpha_rho;
+  a.alpha_stride = 4;
+  a.bcoef = (T)p->B;
+  a.inv_drho = (T)(1.0 / (p->rho_span / p->g.nr));
+  a.inv_dtheta = (T)(1.0 / (p->theta_span / p->g.nt));
+  return a;
+}
+
+// One stage of the fused pipeline: c2r(+alpha, +vmax) -> WENO -> r2c -> rho pass.
+template <typename T>
+void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
+  cudaStream_t s = p->stream;
+  // theta c2r of T (stage 1) or T* (stage 2) into v
+  ThetaArgs<T> c = theta_args<T>(p);
+  c.spec_in = (const cplx<T>*)(stage == 1 ? p->t : p->ts);
+  c.phys_out = (T*)p->v;
+  c.upar = (const T*)p->upar;
+  c.step_ctr = p->step_ctr;
+  c.row_off = stage - 1;
+  c.alpha_bits = p->red + (stage - 1);
+  c.vmax_bits = stage == 1 ? p->vmax_hist : nullptr;
+  launch_theta_c2r<T>(c, p->theta_rows, s);
+  if (ev) cudaEventRecord(ev[0], s);
+  // WENO -> b
+  WenoArgs<T> w = weno_args<T>(p);
+  w.step_ctr = p->step_ctr;
+  w.row_off = stage - 1;
+  w.alpha_bits = p->red + (stage - 1);
+  launch_weno<T>(w, s);
+  // theta r2c of b -> bt
+  ThetaArgs<T> r = theta_args<T>(p);
+  r.phys_in = (const T*)p->b;
+  r.spec_out = (cplx<T>*)p->bt;
+  launch_theta_r2c<T>(r, p->theta_rows, s);
+  if (ev) cudaEventRecord(ev[1], s);
+  // rho pass
+  RhoArgs<T> q = rho_args<T>(p);
+  q.in = (const cplx<T>*)p->bt;
+  int mode;
+  if (scheme == NWB_SCHEME_EXPEULER) {
+    mode = RHO_EULER;
+    q.out = (cplx<T>*)p->t;
+    q.step_ctr = p->step_ctr;
+    q.zero_bits = p->red + 0;
+  } else if (stage == 1) {
+    mode = RHO_STAGE1;
+    q.out = (cplx<T>*)p->ts;
+    q.zero_bits = p->red + 1;
+  } else {
+    mode = RHO_STAGE2;
+    q.out = (cplx<T>*)p->t;
+    q.step_ctr = p->step_ctr;
+    q.zero_bits = p->red + 0;
+  }
+  launch_rho<T>(q, mode, p->rho_threads, s);
+}
+
+template <typename T> void launch_step(nwb_plan* p, int scheme, cudaEvent_t* ev) {
+  if (ev) cudaEventRecord(ev[0], p->stream);
+  launch_stage<T>(p, 1, scheme, ev ? ev + 1 : nullptr);
+  if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev ? ev + 3 : nullptr);
+  if (ev) cudaEventRecord(ev[5], p->stream);
+}
+
+int set_step(nwb_plan* p, int n) {
+  CU(cudaMemcpyAsync(p->step_ctr, &n, sizeof(int), cudaMemcpyHostToDevice, p->stream));
+  CU(cudaStreamSynchronize(p->stream));
+  return NWB_OK;
+}
+
+int check_plan(nwb_plan* p) {
+  if (!p) return fail(NWB_EINVAL, "null plan");
+  CU(cudaSetDevice(p->device));
+  return NWB_OK;
+}
+
+template <typename T> int create_impl(nwb_plan* p) {
+  const Geom& g = p->g;
+  const size_t C = sizeof(cplx<T>);
+  const size_t spec = (size_t)g.batch * g.kk * g.ld * C;
+  const size_t phys = (size_t)g.batch * g.nr * g.nt * sizeof(T);
+  const size_t tab = (size_t)g.kk * g.ld * C;
+  TRY(dalloc(p, &p->vh, spec));
+  TRY(dalloc(p, &p->u, spec));
+  TRY(dalloc(p, &p->t, spec));
+  TRY(dalloc(p, &p->ts, spec));
+  TRY(dalloc(p, &p->bt, spec));
+  TRY(dalloc(p, &p->v, phys));
+  TRY(dalloc(p, &p->b, phys));
+  TRY(dalloc(p, &p->E, tab));
+  TRY(dalloc(p, &p->P1, tab));
+  TRY(dalloc(p, &p->P12, tab));
+  TRY(dalloc(p, &p->P2, tab));
+  TRY(dalloc(p, (void**)&p->red, (size_t)g.batch * 4 * sizeof(u64)));
+  TRY(dalloc(p, (void**)&p->step_ctr, sizeof(int)));
+  CU(cudaMemsetAsync(p->red, 0, (size_t)g.batch * 4 * sizeof(u64), p->stream));
+  CU(cudaMemsetAsync(p->step_ctr, 0, sizeof(int), p->stream));
+  // zero the padding columns once so nothing uninitialised is ever read
+  for (void* a : {p->vh, p->u, p->t, p->ts, p->bt}) CU(cudaMemsetAsync(a, 0, spec, p->stream));
+
+  // twiddles and digit-reversal maps
+  auto twr = twiddles<T>(g.nr, g.nr);
+  auto twh = twiddles<T>(g.m, g.m);
+  auto wk = twiddles<T>(g.nt, g.kk);
+  auto fr = freq_of_pos(p->dr);
+  std::vector<int> pr(g.nr);
+  for (int q = 0; q < g.nr; ++q) pr[fr[q]] = q;
+  auto fh = freq_of_pos(p->dh);
+  std::vector<int> ph(g.m);
+  for (int q = 0; q < g.m; ++q) ph[fh[q]] = q;
+  TRY(dalloc(p, &p->tw_r, twr.size() * C));
+  TRY(dalloc(p, &p->tw_h, twh.size() * C));
+  TRY(dalloc(p, &p->wk, wk.size() * C));
+  TRY(dalloc(p, (void**)&p->pos_r, pr.size() * sizeof(int)));
+  TRY(dalloc(p, (void**)&p->rev_r, fr.size() * sizeof(int)));
+  TRY(dalloc(p, (void**)&p->pos_h, ph.size() * sizeof(int)));
+  CU(cudaMemcpy(p->tw_r, twr.data(), twr.size() * C, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(p->tw_h, twh.data(), twh.size() * C, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(p->wk, wk.data(), wk.size() * C, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(p->pos_r, pr.data(), pr.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(p->rev_r, fr.data(), fr.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(p->pos_h, ph.data(), ph.size() * sizeof(int), cudaMemcpyHostToDevice));
+
+  // multiplier tables, digit-reversed rho order (exprk.py:111-131)
+  TableArgs ta{};
+  ta.nr = g.nr; ta.nt = g.nt; ta.kk = g.kk; ta.ld = g.ld;
+  ta.rho_span = p->rho_span; ta.theta_span = p->theta_span;
+  ta.d_sigma = p->d_sigma; ta.A = p->A; ta.eps = p->eps;
+  ta.rev_r = p->rev_r; ta.natural = 0;
+  CU(cudaMemsetAsync(p->E, 0, tab, p->stream));
+  CU(cudaMemsetAsync(p->P1, 0, tab, p->stream));
+  CU(cudaMemsetAsync(p->P12, 0, tab, p->stream));
+  CU(cudaMemsetAsync(p->P2, 0, tab, p->stream));
+  launch_tables<T>(ta, (cplx<T>*)p->E, (cplx<T>*)p->P1, (cplx<T>*)p->P2, (cplx<T>*)p->P12,
+                   nullptr, p->stream);
+  CHECK_LAUNCH("tables");
+  CU(cudaStreamSynchronize(p->stream));
+  return NWB_OK;
+}
+
+template <typename T> int set_coeffs_impl(nwb_plan* p, const double* up, const double* uq,
+                                          const double* du, int n_rows, int ld, int on_dev) {
+  const Geom& g = p->g;
+  const size_t n = (size_t)n_rows * g.nr;
+  for (void* a : {p->upar, p->uperp, p->du, (void*)p->alpha_rho}) {
+    if (a) {
+      cudaFree(a);
+      for (auto& x : p->allocs)
+        if (x == a) x = nullptr;
+    }
+  }
+  p->upar = p->uperp = p->du = nullptr;
+  p->alpha_rho = nullptr;
+  TRY(dalloc(p, &p->upar, n * sizeof(T)));
+  TRY(dalloc(p, &p->uperp, n * sizeof(T)));
+  TRY(dalloc(p, &p->du, n * sizeof(T)));
+  TRY(dalloc(p, (void**)&p->alpha_rho, (size_t)n_rows * sizeof(double)));
+  p->n_rows = n_rows;
+  double* stage = nullptr;
+  CU(cudaMalloc(&stage, n * sizeof(double)));
+  const double* srcs[3] = {up, uq, du};
+  void* dsts[3] = {p->upar, p->uperp, p->du};
+  for (int i = 0; i < 3; ++i) {
+    if (!srcs[i]) {
+      cudaMemsetAsync(dsts[i], 0, n * sizeof(T), p->stream);
+      continue;
+    }
+    cudaMemcpy2DAsync(stage, g.nr * sizeof(double), srcs[i], (size_t)ld * sizeof(double),
+                      g.nr * sizeof(double), n_rows,
+                      on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, p->stream);
+    launch_convert<T>((long)n, stage, (T*)dsts[i], p->stream);
+  }
+  launch_alpha_rho<T>((const T*)p->uperp, g.nr, n_rows, p->alpha_rho, p->stream);
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  cudaFree(stage);
+  if (e != cudaSuccess) return fail(NWB_ECUDA, std::string("set_coeffs: ") + cudaGetErrorString(e));
+  CHECK_LAUNCH("set_coeffs");
+  return NWB_OK;
+}
+
+template <typename T> int load_physical_impl(nwb_plan* p, const void* v0) {
+  ThetaArgs<T> r = theta_args<T>(p);
+  r.phys_in = (const T*)v0;
+  r.spec_out = (cplx<T>*)p->bt;
+  launch_theta_r2c<T>(r, p->theta_rows, p->stream);
+  RhoArgs<T> q = rho_args<T>(p);
+  q.in = (const cplx<T>*)p->bt;
+  q.out = (cplx<T>*)p->t;
+  launch_rho<T>(q, RHO_INIT, p->rho_threads, p->stream);
+  CHECK_LAUNCH("load_physical");
+  return NWB_OK;
+}
+
+template <typename T> int load_spectrum_impl(nwb_plan* p, const void* vhat) {
+  launch_transpose<T>(p->g, (const cplx<T>*)vhat, (cplx<T>*)p->bt, 0, p->stream);
+  RhoArgs<T> q = rho_args<T>(p);
+  q.in = (const cplx<T>*)p->bt;
+  q.out = (cplx<T>*)p->t;
+  launch_rho<T>(q, RHO_INV_NAT, p->rho_threads, p->stream);
+  CHECK_LAUNCH("load_spectrum");
+  return NWB_OK;
+}
+
+template <typename T> int store_spectrum_impl(nwb_plan* p, void* out) {
+  RhoArgs<T> q = rho_args<T>(p);
+  q.in = (const cplx<T>*)p->vh;
+  q.out = (cplx<T>*)p->bt;
+  launch_rho<T>(q, RHO_REV2NAT, p->rho_threads, p->stream);
+  launch_transpose<T>(p->g, (const cplx<T>*)p->bt, (cplx<T>*)out, 1, p->stream);
+  CHECK_LAUNCH("store_spectrum");
+  return NWB_OK;
+}
+
+template <typename T> int c2r_out(nwb_plan* p, const void* spec, void* out, double* max_abs) {
+  ThetaArgs<T> c = theta_args<T>(p);
+  c.spec_in = (const cplx<T>*)spec;
+  c.phys_out = (T*)out;
+  if (max_abs) {
+    CU(cudaMemsetAsync(p->red, 0, (size_t)p->g.batch * 4 * sizeof(u64), p->stream));
+    c.vmax_bits = p->red + 2;  // slot 2 per member (stride 4, step 0)
+    c.vmax_stride = 4;
+  }
+  launch_theta_c2r<T>(c, p->theta_rows, p->stream);
+  CHECK_LAUNCH("c2r");
+  if (max_abs) {
+    std::vector<u64> h((size_t)p->g.batch * 4);
+    CU(cudaMemcpyAsync(h.data(), p->red, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, p->stream));
+    CU(cudaStreamSynchronize(p->stream));
+    for (int i = 0; i < p->g.batch; ++i) {
+      double d;
+      std::memcpy(&d, &h[(size_t)i * 4 + 2], sizeof(double));
+      max_abs[i] = d;
+    }
+    CU(cudaMemsetAsync(p->red, 0, (size_t)p->g.batch * 4 * sizeof(u64), p->stream));
+  }
+  return NWB_OK;
+}
+
+template <typename T> int rfft2_impl(nwb_plan* p, const void* in, void* out) {
+  ThetaArgs<T> r = theta_args<T>(p);
+  r.phys_in = (const T*)in;
+  r.spec_out = (cplx<T>*)p->bt;
+  launch_theta_r2c<T>(r, p->theta_rows, p->stream);
+  RhoArgs<T> q = rho_args<T>(p);
+  q.in = (const cplx<T>*)p->bt;
+  q.out = (cplx<T>*)p->ts;
+  launch_rho<T>(q, RHO_FWD_NAT, p->rho_threads, p->stream);
+  launch_transpose<T>(p->g, (const cplx<T>*)p->ts, (cplx<T>*)out, 1, p->stream);
+  CHECK_LAUNCH("rfft2");
+  return NWB_OK;
+}
+
+template <typename T> int irfft2_impl(nwb_plan* p, const void* in, void* out) {
+  launch_transpose<T>(p->g, (const cplx<T>*)in, (cplx<T>*)p->bt, 0, p->stream);
+  RhoArgs<T> q = rho_args<T>(p);
+  q.in = (const cplx<T>*)p->bt;
+  q.out = (cplx<T>*)p->ts;
+  q.vh = nullptr;
+  launch_rho<T>(q, RHO_INV_NAT, p->rho_threads, p->stream);
+  CHECK_LAUNCH("irfft2");
+  return c2r_out<T>(p, p->ts, out, nullptr);
+}
+
+// workspace: [batch] u64 alpha_theta bits followed by one double alpha_rho
+template <typename T> int weno_impl(const Geom& g, const void* v, const void* up, const void* uq,
+                                    const void* du, double b, double d_rho, double d_theta,
+                                    void* out, void* ws, cudaStream_t s) {
+  u64* abits = (u64*)ws;
+  double* arho = (double*)(abits + g.batch);
+  CU(cudaMemsetAsync(abits, 0, (size_t)g.batch * sizeof(u64), s));
+  launch_alpha_theta<T>(g, (const T*)v, (const T*)up, (T)b, abits, 1, s);
+  launch_alpha_rho<T>((const T*)uq, g.nr, 1, arho, s);
+  WenoArgs<T> w{};
+  w.g = g;
+  w.v = (const T*)v;
+  w.out = (T*)out;
+  w.upar = (const T*)up;
+  w.uperp = (const T*)uq;
+  w.du = (const T*)du;
+  w.alpha_rho = arho;
+  w.step_ctr = nullptr;
+  w.row_off = 0;
+  w.alpha_bits = abits;
+  w.alpha_stride = 1;
+  w.bcoef = (T)b;
+  w.inv_drho = (T)(1.0 / d_rho);
+  w.inv_dtheta = (T)(1.0 / d_theta);
+  launch_weno<T>(w, s);
+  CHECK_LAUNCH("weno5_b");
+  return NWB_OK;
+}
+
+template <typename T> int step_impl(nwb_plan* p, int scheme, cudaEvent_t* ev) {
+  launch_step<T>(p, scheme, ev);
+  CHECK_LAUNCH("step");
+  return NWB_OK;
+}
+
+template <typename T> int graph_for(nwb_plan* p, int scheme) {
+  const int gi = scheme == NWB_SCHEME_EXPRK22 ? 0 : 1;
+  if (p->graph[gi] && p->graph_stream[gi] == p->stream) return NWB_OK;
+  if (p->graph[gi]) {
+    cudaGraphExecDestroy(p->graph[gi]);
+    p->graph[gi] = nullptr;
+  }
+  cudaGraph_t gr;
+  CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  launch_step<T>(p, scheme, nullptr);
+  cudaError_t le = cudaGetLastError();
+  CU(cudaStreamEndCapture(p->stream, &gr));
+  if (le != cudaSuccess) return fail(NWB_ECUDA, std::string("graph capture: ") + cudaGetErrorString(le));
+  CU(cudaGraphInstantiate(&p->graph[gi], gr, 0));
+  cudaGraphDestroy(gr);
+  p->graph_stream[gi] = p->stream;
+  return NWB_OK;
+}
+
+template <typename T>
+int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, double max_seconds,
+               const int* snap_steps, int n_snap, void* const* snap_bufs, double* max_abs,
+               float* step_ms, int* fail_step, int* fail_member, double* fail_value) {
+  const Geom& g = p->g;
+  if (n_steps <= 0) return NWB_OK;
+  if (!p->upar) return fail(NWB_EINVAL, "coefficients not set (nwb_plan_set_coeffs)");
+  const int need_rows = n0 + n_steps + (scheme == NWB_SCHEME_EXPRK22 ? 1 : 0);
+  if (need_rows > p->n_rows)
+    return fail(NWB_EINVAL, "coefficient rows do not cover the march (" + std::to_string(need_rows) +
+                                " > " + std::to_string(p->n_rows) + ")");
+  // per-step guard history
+  if (p->hist_len < n0 + n_steps) {
+    if (p->vmax_hist) {
+      cudaFree(p->vmax_hist);
+      for (auto& x : p->allocs)
+        if (x == p->vmax_hist) x = nullptr;
+    }
+    p->vmax_hist = nullptr;
+    p->hist_len = n0 + n_steps;
+    TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)g.batch * p->hist_len * sizeof(u64)));
+    for (int i = 0; i < 2; ++i)
+      if (p->graph[i]) {
+        cudaGraphExecDestroy(p->graph[i]);
+        p->graph[i] = nullptr;
+      }
+  }
+  CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)g.batch * p->hist_len * sizeof(u64), p->stream));
+  CU(cudaMemsetAsync(p->red, 0, (size_t)g.batch * 4 * sizeof(u64), p->stream));
+  TRY(set_step(p, n0));
+  const bool use_graph = step_ms == nullptr;
+  if (use_graph) TRY(graph_for<T>(p, scheme));
+
+  std::vector<cudaEvent_t> evs;
+  if (step_ms) {
+    evs.resize((size_t)n_steps * 6);
+    for (auto& e : evs) CU(cudaEventCreate(&e));
+  }
+  auto destroy_events = [&]() {
+    for (auto& e : evs) cudaEventDestroy(e);
+    evs.clear();
+  };
+  const auto t_start = std::chrono::steady_clock::now();
+  const int chunk = max_seconds > 0 ? 8 : 64;
+  std::vector<u64> hbuf;
+  int rc = NWB_OK;
+  int done = 0;
+  while (done < n_steps && rc == NWB_OK) {
+    const int cnt = std::min(chunk, n_steps - done);
+    for (int i = 0; i < cnt; ++i) {
+      const int n = n0 + done + i;
+      int snap = -1;
+      for (int q = 0; q < n_snap; ++q)
+        if (snap_steps[q] == n) snap = q;
+      if (step_ms) {
+        cudaEvent_t* ev = &evs[(size_t)(done + i) * 6];
+        cudaEventRecord(ev[0], p->stream);
+        launch_stage<T>(p, 1, scheme, ev + 1);
+        if (snap >= 0)
+          cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
+                          cudaMemcpyDeviceToDevice, p->stream);
+        if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev + 3);
+        cudaEventRecord(ev[5], p->stream);
+      } else if (snap >= 0) {
+        launch_stage<T>(p, 1, scheme, nullptr);
+        cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
+                        cudaMemcpyDeviceToDevice, p->stream);
+        if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, nullptr);
+      } else {
+        cudaError_t e = cudaGraphLaunch(p->graph[scheme == NWB_SCHEME_EXPRK22 ? 0 : 1], p->stream);
+        if (e != cudaSuccess) {
+          destroy_events();
+          return fail(NWB_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+        }
+      }
+    }
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) {
+      destroy_events();
+      return fail(NWB_ECUDA, std::string("march launch: ") + cudaGetErrorString(le));
+    }
+    // guard check on this chunk (host sync)
+    hbuf.resize((size_t)g.batch * cnt);
+    for (int mbr = 0; mbr < g.batch; ++mbr)
+      cudaMemcpyAsync(hbuf.data() + (size_t)mbr * cnt, p->vmax_hist + (size_t)mbr * p->hist_len + n0 + done,
+                      cnt * sizeof(u64), cudaMemcpyDeviceToHost, p->stream);
+    cudaError_t se = cudaStreamSynchronize(p->stream);
+    if (se != cudaSuccess) {
+      destroy_events();
+      return fail(NWB_ECUDA, std::string("march: ") + cudaGetErrorString(se));
+    }
+    for (int i = 0; i < cnt && rc == NWB_OK; ++i) {
+      for (int mbr = 0; mbr < g.batch; ++mbr) {
+        double m;
+        std::memcpy(&m, &hbuf[(size_t)mbr * cnt + i], sizeof(double));
+        if (max_abs) max_abs[(size_t)mbr * n_steps + done + i] = m;
+        if (!(std::isfinite(m) && m <= guard)) {
+          if (fail_step) *fail_step = n0 + done + i;
+          if (fail_member) *fail_member = mbr;
+          if (fail_value) *fail_value = m;
+          rc = fail(NWB_EINSTABILITY, "max|V| left the guard");
+          break;
+        }
+      }
+    }
+    done += cnt;
+    if (rc == NWB_OK && max_seconds > 0) {
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+      if (el > max_seconds && done < n_steps) {
+        if (fail_step) *fail_step = n0 + done;
+        rc = fail(NWB_EBUDGET, "wall-clock budget exhausted");
+      }
+    }
+  }
+  if (step_ms) {
+    const int ran = done;
+    for (int i = 0; i < ran; ++i) {
+      cudaEvent_t* ev = &evs[(size_t)i * 6];
+      float tot = 0, a = 0, b = 0, c = 0, d = 0;
+      cudaEventElapsedTime(&tot, ev[0], ev[5]);
+      cudaEventElapsedTime(&a, ev[1], ev[2]);  // WENO + r2c, stage 1
+      if (scheme == NWB_SCHEME_EXPRK22) cudaEventElapsedTime(&b, ev[3], ev[4]);
+      (void)c; (void)d;
+      step_ms[(size_t)i * 3 + 0] = tot;
+      step_ms[(size_t)i * 3 + 1] = a + b;
+      step_ms[(size_t)i * 3 + 2] = tot - (a + b);
+    }
+    destroy_events();
+  }
+  return rc;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+int nwb_abi_version(void) { return 1; }
+
+const char* nwb_last_error(void) { return g_err.c_str(); }
+
+int nwb_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int precision,
+                    double d_sigma, double rho_span, double theta_span, double A, double B,
+                    double eps, int device) {
+  if (!out) return fail(NWB_EINVAL, "null plan pointer");
+  *out = nullptr;
+  if (n_rho < 1 || n_theta < 2 || batch < 1) return fail(NWB_EINVAL, "grid extents must be positive");
+  if (precision != NWB_F64 && precision != NWB_F32) return fail(NWB_EINVAL, "unknown precision");
+  if (n_theta % 2) return fail(NWB_EUNSUPPORTED, "n_theta must be even (half-length real FFT)");
+  nwb_plan* p = new nwb_plan();
+  p->device = device;
+  p->prec = precision;
+  p->rsz = precision == NWB_F64 ? 8 : 4;
+  p->g.nr = n_rho;
+  p->g.nt = n_theta;
+  p->g.m = n_theta / 2;
+  p->g.kk = n_theta / 2 + 1;
+  p->g.ld = (n_rho + 7) / 8 * 8;
+  p->g.batch = batch;
+  p->d_sigma = d_sigma;
+  p->rho_span = rho_span;
+  p->theta_span = theta_span;
+  p->A = A;
+  p->B = B;
+  p->eps = eps;
+  if (!factorize(n_rho, p->dr) || !factorize(p->g.m, p->dh)) {
+    delete p;
+    return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
+  }
+  const size_t csz = 2 * p->rsz;
+  const size_t smem_max = 227 * 1024;
+  if ((size_t)n_rho * csz > smem_max || (size_t)p->g.m * csz > smem_max) {
+    delete p;
+    return fail(NWB_EUNSUPPORTED, "transform length exceeds one CTA's shared memory");
+  }
+  const size_t row_bytes = (size_t)p->g.m * csz;
+  p->theta_rows = 1;
+  for (int r : {8, 4, 2})
+    if ((size_t)r * row_bytes <= 64 * 1024) {
+      p->theta_rows = r;
+      break;
+    }
+  int th = ((n_rho / 4) + 31) / 32 * 32;
+  p->rho_threads = th < 64 ? 64 : (th > 512 ? 512 : th);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(NWB_ECUDA, std::string("plan device/stream: ") + cudaGetErrorString(e));
+  }
+  p->stream = p->own_stream;
+  int rc = precision == NWB_F64 ? create_impl<double>(p) : create_impl<float>(p);
+  if (rc != NWB_OK) {
+    nwb_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return NWB_OK;
+}
+
+int nwb_plan_destroy(nwb_plan* p) {
+  if (!p) return NWB_OK;
+  cudaSetDevice(p->device);
+  cudaStreamSynchronize(p->stream);
+  for (int i = 0; i < 2; ++i)
+    if (p->graph[i]) cudaGraphExecDestroy(p->graph[i]);
+  for (void* a : p->allocs)
+    if (a) cudaFree(a);
+  if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  delete p;
+  return NWB_OK;
+}
+
+int nwb_plan_set_stream(nwb_plan* p, void* stream) {
+  TRY(check_plan(p));
+  p->stream = stream ? (cudaStream_t)stream : p->own_stream;
+  return NWB_OK;
+}
+
+long long nwb_plan_bytes(const nwb_plan* p) { return p ? p->bytes : 0; }
+
+int nwb_plan_set_coeffs(nwb_plan* p, const double* u_par, const double* u_perp,
+                        const double* du_drho, int n_rows, int ld, int on_device) {
+  TRY(check_plan(p));
+  if (n_rows < 1 || ld < p->g.nr) return fail(NWB_EINVAL, "coefficient rows / ld too small");
+  return p->prec == NWB_F64 ? set_coeffs_impl<double>(p, u_par, u_perp, du_drho, n_rows, ld, on_device)
+                            : set_coeffs_impl<float>(p, u_par, u_perp, du_drho, n_rows, ld, on_device);
+}
+
+int nwb_plan_load_physical(nwb_plan* p, const void* v0) {
+  TRY(check_plan(p));
+  return p->prec == NWB_F64 ? load_physical_impl<double>(p, v0) : load_physical_impl<float>(p, v0);
+}
+
+int nwb_plan_load_spectrum(nwb_plan* p, const void* vhat) {
+  TRY(check_plan(p));
+  return p->prec == NWB_F64 ? load_spectrum_impl<double>(p, vhat) : load_spectrum_impl<float>(p, vhat);
+}
+
+int nwb_plan_store_spectrum(nwb_plan* p, void* vhat) {
+  TRY(check_plan(p));
+  return p->prec == NWB_F64 ? store_spectrum_impl<double>(p, vhat) : store_spectrum_impl<float>(p, vhat);
+}
+
+int nwb_plan_store_physical(nwb_plan* p, void* v, double* max_abs) {
+  TRY(check_plan(p));
+  return p->prec == NWB_F64 ? c2r_out<double>(p, p->t, v, max_abs) : c2r_out<float>(p, p->t, v, max_abs);
+}
+
+int nwb_march(nwb_plan* p, int scheme, int n0, int n_steps, double guard, double max_seconds,
+              const int* snap_steps, int n_snap, void* const* snap_bufs, double* max_abs,
+              float* step_ms, int* fail_step, int* fail_member, double* fail_value) {
+  TRY(check_plan(p));
+  if (scheme != NWB_SCHEME_EXPRK22 && scheme != NWB_SCHEME_EXPEULER) return fail(NWB_EINVAL, "unknown scheme");
+  if (n0 < 0 || n_steps < 0) return fail(NWB_EINVAL, "negative step range");
+  return p->prec == NWB_F64
+             ? march_impl<double>(p, scheme, n0, n_steps, guard, max_seconds, snap_steps, n_snap,
+                                  snap_bufs, max_abs, step_ms, fail_step, fail_member, fail_value)
+             : march_impl<float>(p, scheme, n0, n_steps, guard, max_seconds, snap_steps, n_snap,
+                                 snap_bufs, max_abs, step_ms, fail_step, fail_member, fail_value);
+}
+
+int nwb_step(nwb_plan* p, int scheme, int n) {
+  TRY(check_plan(p));
+  if (!p->upar) return fail(NWB_EINVAL, "coefficients not set");
+  if (n + (scheme == NWB_SCHEME_EXPRK22 ? 1 : 0) >= p->n_rows) return fail(NWB_EINVAL, "coefficient rows do not cover the step");
+  if (p->hist_len < n + 1) {
+    if (p->vmax_hist) {
+      cudaFree(p->vmax_hist);
+      for (auto& x : p->allocs)
+        if (x == p->vmax_hist) x = nullptr;
+    }
+    p->vmax_hist = nullptr;
+    p->hist_len = n + 1;
+    TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)p->g.batch * p->hist_len * sizeof(u64)));
+    CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)p->g.batch * p->hist_len * sizeof(u64), p->stream));
+  }
+  TRY(set_step(p, n));
+  return p->prec == NWB_F64 ? step_impl<double>(p, scheme, nullptr) : step_impl<float>(p, scheme, nullptr);
+}
+
+int nwb_rfft2(nwb_plan* p, const void* in, void* out) {
+  TRY(check_plan(p));
+  return p->prec == NWB_F64 ? rfft2_impl<double>(p, in, out) : rfft2_impl<float>(p, in, out);
+}
+
+int nwb_irfft2(nwb_plan* p, const void* in, void* out) {
+  TRY(check_plan(p));
+  return p->prec == NWB_F64 ? irfft2_impl<double>(p, in, out) : irfft2_impl<float>(p, in, out);
+}
+
+int nwb_weno5_b(int precision, int batch, int n_rho, int n_theta, const void* v, const void* up,
+                const void* uq, const void* du, double b, double d_rho, double d_theta, void* out,
+                void* workspace, void* stream) {
+  if (batch < 1 || n_rho < 1 || n_theta < 1) return fail(NWB_EINVAL, "grid extents must be positive");
+  if (!v || !up || !uq || !du || !out || !workspace) return fail(NWB_EINVAL, "null buffer");
+  Geom g{};
+  g.nr = n_rho;
+  g.nt = n_theta;
+  g.batch = batch;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == NWB_F64) return weno_impl<double>(g, v, up, uq, du, b, d_rho, d_theta, out, workspace, s);
+  if (precision == NWB_F32) return weno_impl<float>(g, v, up, uq, du, b, d_rho, d_theta, out, workspace, s);
+  return fail(NWB_EINVAL, "unknown precision");
+}
+
+int nwb_tables(int precision, int n_rho, int n_theta, double rho_span, double theta_span,
+               double d_sigma, double A, double eps, void* E, void* P1, void* P2, void* P12,
+               void* z, void* stream) {
+  if (n_rho < 1 || n_theta < 1) return fail(NWB_EINVAL, "grid extents must be positive");
+  TableArgs ta{};
+  ta.nr = n_rho; ta.nt = n_theta; ta.kk = n_theta / 2 + 1; ta.ld = ta.kk;
+  ta.rho_span = rho_span; ta.theta_span = theta_span; ta.d_sigma = d_sigma; ta.A = A; ta.eps = eps;
+  ta.rev_r = nullptr; ta.natural = 1;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == NWB_F64)
+    launch_tables<double>(ta, (double2*)E, (double2*)P1, (double2*)P2, (double2*)P12, (double2*)z, s);
+  else
+    launch_tables<float>(ta, (float2*)E, (float2*)P1, (float2*)P2, (float2*)P12, (double2*)z, s);
+  CHECK_LAUNCH("tables");
+  return NWB_OK;
+}
+
+int nwb_phi(const void* z, long long n, int shift, void* out, void* stream) {
+  if (shift != 1 && shift != 2) return fail(NWB_EINVAL, "phi shift must be 1 or 2");
+  if (n <= 0) return NWB_OK;
+  launch_phi((const double2*)z, (long)n, shift, (double2*)out, (cudaStream_t)stream);
+  CHECK_LAUNCH("phi");
+  return NWB_OK;
+}
+
+int nwb_combine(int precision, long long n, int mode, double ds, const void* E, const void* P1,
+                const void* P12, const void* P2, const void* vh, const void* b1, const void* b2,
+                void* out, void* stream) {
+  if (mode < 0 || mode > 3) return fail(NWB_EINVAL, "unknown combine mode");
+  if (n <= 0) return NWB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == NWB_F64)
+    launch_combine<double>((long)n, mode, ds, (const double2*)E, (const double2*)P1, (const double2*)P12,
+                           (const double2*)P2, (const double2*)vh, (const double2*)b1,
+                           (const double2*)b2, (double2*)out, s);
+  else
+    launch_combine<float>((long)n, mode, ds, (const float2*)E, (const float2*)P1, (const float2*)P12,
+                          (const float2*)P2, (const float2*)vh, (const float2*)b1, (const float2*)b2,
+                          (float2*)out, s);
+  CHECK_LAUNCH("combine");
+  return NWB_OK;
+}
+
+}  // extern "C"

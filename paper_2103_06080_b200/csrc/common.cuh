@@ -1,0 +1,51 @@
+// Shared device helpers: complex arithmetic on double2/float2, ordered-bit
+// max reductions, launch checking.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nwb {
+
+template <typename T> struct cplx_of;
+template <> struct cplx_of<double> { using type = double2; };
+template <> struct cplx_of<float> { using type = float2; };
+template <typename T> using cplx = typename cplx_of<T>::type;
+
+template <typename V> __device__ __forceinline__ V mk(decltype(V::x) re, decltype(V::x) im) {
+  V r; r.x = re; r.y = im; return r;
+}
+template <typename V> __device__ __forceinline__ V cadd(V a, V b) { return mk<V>(a.x + b.x, a.y + b.y); }
+template <typename V> __device__ __forceinline__ V csub(V a, V b) { return mk<V>(a.x - b.x, a.y - b.y); }
+template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
+  return mk<V>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename V> __device__ __forceinline__ V cmulc(V a, V b) {
+  return mk<V>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename V> __device__ __forceinline__ V cconj(V a) { return mk<V>(a.x, -a.y); }
+template <typename V> __device__ __forceinline__ V cscale(V a, decltype(V::x) s) { return mk<V>(a.x * s, a.y * s); }
+// multiply by +i (INV=true) or -i (INV=false)
+template <bool PLUS, typename V> __device__ __forceinline__ V mul_i(V a) {
+  return PLUS ? mk<V>(-a.y, a.x) : mk<V>(a.y, -a.x);
+}
+
+// Max of non-negative values (and NaN) through the IEEE bit pattern: for
+// x >= 0 the unsigned bit pattern orders like the value, and any NaN with
+// the sign bit cleared sorts above +inf, so a NaN anywhere wins the max.
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  return (unsigned long long)__double_as_longlong(x) & 0x7fffffffffffffffULL;
+}
+__device__ __forceinline__ unsigned long long abs_bits(float x) {
+  return abs_bits((double)x);
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+}  // namespace nwb

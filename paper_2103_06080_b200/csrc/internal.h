@@ -1,0 +1,119 @@
+// Host-side declarations shared by the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fft.cuh"
+
+namespace nwb {
+
+typedef unsigned long long u64;
+
+// rho-pass modes
+enum RhoMode {
+  RHO_STAGE1 = 0,   // B1 = F(bt); U = E V + ds P12 B1; V* = E V + ds P1 B1 -> T* = F^-1 V*
+  RHO_STAGE2 = 1,   // B2 = F(bt); V+ = U + ds P2 B2 -> Vh, T = F^-1 V+
+  RHO_EULER = 2,    // B1 = F(bt); V+ = E V + ds P1 B1 -> Vh, T
+  RHO_INIT = 3,     // Vh = F(bt) (digit-reversed), T = F^-1 Vh
+  RHO_FWD_NAT = 4,  // out = F(bt) in natural order (no inverse)
+  RHO_INV_NAT = 5,  // out = F^-1(in), `in` in natural order (vh = in, digit-reversed, if set)
+  RHO_REV2NAT = 6,  // out = in permuted from digit-reversed to natural order
+};
+
+// Geometry of one plan: physical fields are (batch, nr, nt) real, spectral
+// arrays (batch, kk, ld) complex with kk = nt/2 + 1 rows of the rho axis.
+struct Geom {
+  int nr, nt, m, kk, ld, batch;
+};
+
+template <typename T> struct ThetaArgs {
+  Geom g;
+  FftDesc dh;                 // half-length (m) complex transform
+  const cplx<T>* tw_h;        // W_m^t
+  const cplx<T>* wk;          // W_nt^k, k <= m
+  const int* pos_h;           // frequency -> position (digit reversal), length m
+  // c2r: spectral (kk, ld) -> physical; r2c: physical -> spectral (kk, ld)
+  const cplx<T>* spec_in;
+  cplx<T>* spec_out;
+  const T* phys_in;
+  T* phys_out;
+  T scale;                    // c2r output scale (1 / (nr nt))
+  // optional reductions (c2r): alpha = max|2 pi u_par[j] + B v|, vmax = max|v|
+  const T* upar;              // coefficient table base (rows of nr) or null
+  const int* step_ctr;        // device step counter (row = *step_ctr + row_off) or null
+  int row_off;
+  T bcoef;
+  u64* alpha_bits;            // per member, stride alpha_stride, or null
+  int alpha_stride;
+  u64* vmax_bits;             // per member, stride vmax_stride, slot = *step_ctr, or null
+  int vmax_stride;
+};
+
+template <typename T> struct RhoArgs {
+  Geom g;
+  FftDesc dr;
+  const cplx<T>* tw_r;
+  const int* pos_r;           // frequency -> position
+  const cplx<T>* in;          // (batch, kk, ld)
+  cplx<T>* out;               // (batch, kk, ld)
+  cplx<T>* vh;                // state spectrum, digit-reversed
+  cplx<T>* u;                 // stage-1 partial update, digit-reversed
+  const cplx<T>* E;           // tables (kk, ld), digit-reversed
+  const cplx<T>* P1;
+  const cplx<T>* P12;
+  const cplx<T>* P2;
+  T ds;
+  int* step_ctr;              // incremented by block (0,0) when non-null (last kernel of a step)
+  u64* zero_bits;             // alpha slot cleared for the next stage (per member), or null
+  int zero_stride;
+};
+
+template <typename T> struct WenoArgs {
+  Geom g;
+  const T* v;
+  T* out;
+  const T* upar;              // coefficient rows (nr each)
+  const T* uperp;
+  const T* du;
+  const double* alpha_rho;    // per coefficient row
+  const int* step_ctr;
+  int row_off;
+  const u64* alpha_bits;      // alpha_theta per member (stride alpha_stride)
+  int alpha_stride;
+  T bcoef;
+  T inv_drho, inv_dtheta;
+};
+
+template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s);
+template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cudaStream_t s);
+template <typename T> void launch_rho(const RhoArgs<T>& a, int mode, int threads, cudaStream_t s);
+template <typename T> void launch_weno(const WenoArgs<T>& a, cudaStream_t s);
+template <typename T>
+void launch_alpha_theta(const Geom& g, const T* v, const T* upar, T bcoef, u64* bits,
+                        int stride, cudaStream_t s);
+template <typename T>
+void launch_alpha_rho(const T* uperp, int nr, int rows, double* out, cudaStream_t s);
+template <typename T>
+void launch_transpose(const Geom& g, const cplx<T>* in, cplx<T>* out, int to_natural,
+                      cudaStream_t s);
+template <typename T>
+void launch_combine(long n, int mode, double ds, const cplx<T>* E, const cplx<T>* P1,
+                    const cplx<T>* P12, const cplx<T>* P2, const cplx<T>* vh,
+                    const cplx<T>* b1, const cplx<T>* b2, cplx<T>* out, cudaStream_t s);
+template <typename T>
+void launch_convert(long n, const double* in, T* out, cudaStream_t s);
+
+// tables.cu (compiled with -fmad=false so the z / exp / phi arithmetic
+// rounds like numpy's)
+struct TableArgs {
+  int nr, nt, kk, ld;
+  double rho_span, theta_span, d_sigma, A, eps;
+  const int* rev_r;           // position -> frequency (plan layout) or null (natural)
+  int natural;                // 1: (nr, kk) row-major frequency order; 0: (kk, ld) digit-reversed
+};
+template <typename T>
+void launch_tables(const TableArgs& a, cplx<T>* E, cplx<T>* P1, cplx<T>* P2, cplx<T>* P12,
+                   double2* z, cudaStream_t s);
+void launch_phi(const double2* z, long n, int shift, double2* out, cudaStream_t s);
+
+}  // namespace nwb

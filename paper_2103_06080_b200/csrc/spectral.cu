@@ -1,0 +1,369 @@
+// Spectral passes of the ExpRK22 step (reference pkg/src/nwave/exprk.py).
+//
+//   theta c2r  -- rows of the rho-physical / theta-spectral state T -> V,
+//                 fused with the LF speed alpha_theta (weno.py:93-103) and the
+//                 divergence guard max|V| (exprk.py:297) reductions.
+//   theta r2c  -- rows of b -> theta spectrum, written transposed.
+//   rho pass   -- one rho column (one theta mode k) per CTA: forward FFT,
+//                 the stage combine of exprk.py:161-173 in digit-reversed
+//                 order, inverse FFT.
+//
+// Data layout in HBM: physical fields are
+// (batch, nr, nt) row-major; spectral arrays are (batch, kk, ld) with the
+// rho index contiguous, so the rho pass streams contiguous rows and the
+// theta passes move R-row segments (R x 16 B fp64) per theta mode.
+#include "internal.h"
+
+namespace nwb {
+
+// ------------------------------------------------------------------ helpers
+
+template <typename T>
+__device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b) {
+  __shared__ u64 red[2][32];
+  a = warp_max_u64(a);
+  b = warp_max_u64(b);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) { red[0][w] = a; red[1][w] = b; }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    a = lane < nw ? red[0][lane] : 0ULL;
+    b = lane < nw ? red[1][lane] : 0ULL;
+    a = warp_max_u64(a);
+    b = warp_max_u64(b);
+    if (lane == 0) {
+      if (dst_a) atomicMax(dst_a, a);
+      if (dst_b) atomicMax(dst_b, b);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ theta c2r
+// X[0..m] (Im of X[0], X[m] dropped as pocketfft's c2r does) ->
+//   Z[k] = (X[k] + conj X[m-k]) + i (X[k] - conj X[m-k]) conj(W_nt^k),  k < m
+// placed at digit-reversed slots, inverse m-point DIT, then
+//   v[2n] = Re z[n] * scale, v[2n+1] = Im z[n] * scale.
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_theta_c2r(const ThetaArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* z = reinterpret_cast<V*>(smem_raw);
+  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
+  const int mem = blockIdx.y;
+  const int j0 = blockIdx.x * R;
+  const V* src = a.spec_in + (size_t)mem * a.g.kk * ld;
+  const int npairs = m / 2 + 1;
+  for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
+    const int r = idx % R, k = idx / R, j = j0 + r;
+    if (j >= nr) continue;
+    V xk = src[(size_t)k * ld + j];
+    V xm = src[(size_t)(m - k) * ld + j];
+    if (k == 0) { xk.y = 0; xm.y = 0; }
+    const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
+    const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), a.wk[k]);
+    z[r * m + a.pos_h[k]] = mk<V>(ze.x - zo.y, ze.y + zo.x);
+    if (k != 0 && 2 * k != m) z[r * m + a.pos_h[m - k]] = mk<V>(ze.x + zo.y, zo.x - ze.y);
+  }
+  __syncthreads();
+  fft_inverse(z, a.dh, R, m, a.tw_h);
+
+  const int step = a.step_ctr ? *a.step_ctr : 0;
+  const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * nr : nullptr;
+  const T two_pi = (T)6.283185307179586476925;
+  u64 amax = 0, vmax = 0;
+  T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
+  for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
+    const int r = idx / m, n = idx - r * m, j = j0 + r;
+    if (j >= nr) continue;
+    const V zz = z[r * m + n];
+    const T v0 = zz.x * a.scale, v1 = zz.y * a.scale;
+    *reinterpret_cast<V*>(dst + (size_t)j * a.g.nt + 2 * n) = mk<V>(v0, v1);
+    const T c = up ? two_pi * up[j] : (T)0;
+    u64 s0 = abs_bits(c + a.bcoef * v0), s1 = abs_bits(c + a.bcoef * v1);
+    u64 q0 = abs_bits(v0), q1 = abs_bits(v1);
+    amax = max(amax, max(s0, s1));
+    vmax = max(vmax, max(q0, q1));
+  }
+  if (a.alpha_bits || a.vmax_bits) {
+    block_max2<T>(amax, vmax,
+                  a.alpha_bits ? a.alpha_bits + (size_t)mem * a.alpha_stride : nullptr,
+                  a.vmax_bits ? a.vmax_bits + (size_t)mem * a.vmax_stride + step : nullptr);
+  }
+}
+
+// ------------------------------------------------------------------ theta r2c
+// z[n] = v[2n] + i v[2n+1]; forward m-point DIF; then for each pair (k, m-k)
+//   ze = (Z_k + conj Z_{m-k}) / 2,  zo = -i (Z_k - conj Z_{m-k}) / 2
+//   X[k] = ze + W_nt^k zo,   X[m-k] = conj(ze - W_nt^k zo).
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_theta_r2c(const ThetaArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* z = reinterpret_cast<V*>(smem_raw);
+  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
+  const int mem = blockIdx.y;
+  const int j0 = blockIdx.x * R;
+  const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
+  for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
+    const int r = idx / m, n = idx - r * m, j = j0 + r;
+    z[idx] = j < nr ? *reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n)
+                    : mk<V>(0, 0);
+  }
+  __syncthreads();
+  fft_forward(z, a.dh, R, m, a.tw_h);
+  V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
+  const int npairs = m / 2 + 1;
+  const T half = (T)0.5;
+  for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
+    const int r = idx % R, k = idx / R, j = j0 + r;
+    if (j >= nr) continue;
+    const V zk = z[r * m + a.pos_h[k]];
+    const V zm = z[r * m + a.pos_h[k == 0 ? 0 : m - k]];
+    const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
+    const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
+    const V wz = cmul(a.wk[k], zo);
+    dst[(size_t)k * ld + j] = cadd(ze, wz);
+    if (2 * k != m) {
+      const V d = csub(ze, wz);
+      dst[(size_t)(m - k) * ld + j] = mk<V>(d.x, -d.y);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ rho pass
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(1024) k_rho(const RhoArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* x = reinterpret_cast<V*>(smem_raw);
+  const int n = a.dr.n;
+  const int mem = blockIdx.x, k = blockIdx.y;
+  const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+  const size_t trow = (size_t)k * a.g.ld;
+  const V* src = a.in + row;
+  if (MODE == RHO_REV2NAT) {
+    V* dst = a.out + row;
+    for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = src[a.pos_r[f]];
+    return;
+  }
+  if (MODE == RHO_INV_NAT) {
+    for (int f = threadIdx.x; f < n; f += blockDim.x) {
+      const int p = a.pos_r[f];
+      const V val = src[f];
+      x[p] = val;
+      if (a.vh) a.vh[row + p] = val;
+    }
+  } else {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) x[j] = src[j];
+  }
+  if (a.zero_bits && k == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
+  __syncthreads();
+  if (MODE != RHO_INV_NAT) fft_forward(x, a.dr, 1, 0, a.tw_r);
+
+  if (MODE == RHO_FWD_NAT) {
+    V* dst = a.out + row;
+    for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = x[a.pos_r[f]];
+    return;
+  }
+  const T ds = a.ds;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const V b = x[p];
+    if (MODE == RHO_STAGE1) {
+      const V ev = cmul(a.E[trow + p], a.vh[row + p]);
+      const V p1 = a.P1[trow + p], p12 = a.P12[trow + p];
+      const V vs = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), b));
+      a.u[row + p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), b));
+      x[p] = vs;
+    } else if (MODE == RHO_STAGE2) {
+      const V p2 = a.P2[trow + p];
+      const V vn = cadd(a.u[row + p], cmul(mk<V>(ds * p2.x, ds * p2.y), b));
+      a.vh[row + p] = vn;
+      x[p] = vn;
+    } else if (MODE == RHO_EULER) {
+      const V p1 = a.P1[trow + p];
+      const V vn = cadd(cmul(a.E[trow + p], a.vh[row + p]), cmul(mk<V>(ds * p1.x, ds * p1.y), b));
+      a.vh[row + p] = vn;
+      x[p] = vn;
+    } else if (MODE == RHO_INIT) {
+      a.vh[row + p] = b;
+    }
+  }
+  __syncthreads();
+  fft_inverse(x, a.dr, 1, 0, a.tw_r);
+  V* dst = a.out + row;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[j];
+  if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+}
+
+// ------------------------------------------------------------------ transpose
+// (kk, ld) [k][j]  <->  (nr, kk) [j][k], per member.
+
+template <typename T>
+__global__ void k_transpose(const Geom g, const cplx<T>* __restrict__ in, cplx<T>* __restrict__ out,
+                            int to_natural) {
+  using V = cplx<T>;
+  __shared__ V tile[32][33];
+  const int mem = blockIdx.z;
+  // to_natural: source rows = k (kk of them), source cols = j (nr)
+  const int srows = to_natural ? g.kk : g.nr;
+  const int scols = to_natural ? g.nr : g.kk;
+  const int sld = to_natural ? g.ld : g.kk;
+  const int dld = to_natural ? g.kk : g.ld;
+  const size_t sbase = (size_t)mem * (to_natural ? (size_t)g.kk * g.ld : (size_t)g.nr * g.kk);
+  const size_t dbase = (size_t)mem * (to_natural ? (size_t)g.nr * g.kk : (size_t)g.kk * g.ld);
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int r = r0 + dy, c = c0 + threadIdx.x;
+    if (r < srows && c < scols) tile[dy][threadIdx.x] = in[sbase + (size_t)r * sld + c];
+  }
+  __syncthreads();
+  for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+    const int r = c0 + dy, c = r0 + threadIdx.x;  // dest row = source col
+    if (r < scols && c < srows) out[dbase + (size_t)r * dld + c] = tile[threadIdx.x][dy];
+  }
+}
+
+// ------------------------------------------------------------------ combine
+// Elementwise spectral combines of the generic step API (exprk.py:166-173,
+// 193) with numpy's complex rounding: explicit _rn intrinsics keep nvcc
+// from contracting into FMAs, so `E * vhat` matches numpy bitwise.
+
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float rn_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float rn_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rn_sub(float a, float b) { return __fsub_rn(a, b); }
+
+template <typename V> __device__ __forceinline__ V np_mul(V a, V b) {
+  return mk<V>(rn_sub(rn_mul(a.x, b.x), rn_mul(a.y, b.y)), rn_add(rn_mul(a.x, b.y), rn_mul(a.y, b.x)));
+}
+template <typename V> __device__ __forceinline__ V np_add(V a, V b) {
+  return mk<V>(rn_add(a.x, b.x), rn_add(a.y, b.y));
+}
+// real scalar * complex as numpy does it: (s + 0j) * a
+template <typename V> __device__ __forceinline__ V np_scale(decltype(V::x) s, V a) {
+  return mk<V>(rn_sub(rn_mul(s, a.x), rn_mul((decltype(V::x))0, a.y)),
+               rn_add(rn_mul(s, a.y), rn_mul((decltype(V::x))0, a.x)));
+}
+
+template <typename T>
+__global__ void k_combine(long n, int mode, T ds, const cplx<T>* E, const cplx<T>* P1,
+                          const cplx<T>* P12, const cplx<T>* P2, const cplx<T>* vh,
+                          const cplx<T>* b1, const cplx<T>* b2, cplx<T>* out) {
+  using V = cplx<T>;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    V r;
+    if (mode == 0) {          // ev = E * vhat
+      r = np_mul(E[i], vh[i]);
+    } else if (mode == 1) {   // vh here is ev: ev + (ds * Phi1) * bh1
+      r = np_add(vh[i], np_mul(np_scale(ds, P1[i]), b1[i]));
+    } else if (mode == 2) {   // ev + ds * (Phi1m2 * bh1 + Phi2 * bh2)
+      r = np_add(vh[i], np_scale(ds, np_add(np_mul(P12[i], b1[i]), np_mul(P2[i], b2[i]))));
+    } else {                  // Euler: E * vhat + (ds * Phi1) * bh1
+      r = np_add(np_mul(E[i], vh[i]), np_mul(np_scale(ds, P1[i]), b1[i]));
+    }
+    out[i] = r;
+  }
+}
+
+template <typename T>
+__global__ void k_convert(long n, const double* in, T* out) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    out[i] = (T)in[i];
+}
+
+// ------------------------------------------------------------------ launchers
+
+static inline int grid_cap(long n, int threads) {
+  long b = (n + threads - 1) / threads;
+  return (int)(b < 148L * 16 ? (b < 1 ? 1 : b) : 148L * 16);
+}
+
+template <typename T, int R>
+static void c2r_r(const ThetaArgs<T>& a, cudaStream_t s) {
+  const size_t sm = (size_t)R * a.g.m * sizeof(cplx<T>);
+  cudaFuncSetAttribute(k_theta_c2r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
+  k_theta_c2r<T, R><<<grid, 256, sm, s>>>(a);
+}
+template <typename T, int R>
+static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
+  const size_t sm = (size_t)R * a.g.m * sizeof(cplx<T>);
+  cudaFuncSetAttribute(k_theta_r2c<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
+  k_theta_r2c<T, R><<<grid, 256, sm, s>>>(a);
+}
+
+template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s) {
+  switch (rows) {
+    case 1: c2r_r<T, 1>(a, s); break;
+    case 2: c2r_r<T, 2>(a, s); break;
+    case 4: c2r_r<T, 4>(a, s); break;
+    default: c2r_r<T, 8>(a, s); break;
+  }
+}
+template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cudaStream_t s) {
+  switch (rows) {
+    case 1: r2c_r<T, 1>(a, s); break;
+    case 2: r2c_r<T, 2>(a, s); break;
+    case 4: r2c_r<T, 4>(a, s); break;
+    default: r2c_r<T, 8>(a, s); break;
+  }
+}
+
+template <typename T, int MODE>
+static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
+  const size_t sm = (size_t)a.dr.n * sizeof(cplx<T>);
+  cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid(a.g.batch, a.g.kk);
+  k_rho<T, MODE><<<grid, threads, sm, s>>>(a);
+}
+
+template <typename T> void launch_rho(const RhoArgs<T>& a, int mode, int threads, cudaStream_t s) {
+  switch (mode) {
+    case RHO_STAGE1: rho_m<T, RHO_STAGE1>(a, threads, s); break;
+    case RHO_STAGE2: rho_m<T, RHO_STAGE2>(a, threads, s); break;
+    case RHO_EULER: rho_m<T, RHO_EULER>(a, threads, s); break;
+    case RHO_INIT: rho_m<T, RHO_INIT>(a, threads, s); break;
+    case RHO_FWD_NAT: rho_m<T, RHO_FWD_NAT>(a, threads, s); break;
+    case RHO_INV_NAT: rho_m<T, RHO_INV_NAT>(a, threads, s); break;
+    default: rho_m<T, RHO_REV2NAT>(a, threads, s); break;
+  }
+}
+
+template <typename T>
+void launch_transpose(const Geom& g, const cplx<T>* in, cplx<T>* out, int to_natural, cudaStream_t s) {
+  const int srows = to_natural ? g.kk : g.nr, scols = to_natural ? g.nr : g.kk;
+  dim3 grid((scols + 31) / 32, (srows + 31) / 32, g.batch);
+  k_transpose<T><<<grid, dim3(32, 8), 0, s>>>(g, in, out, to_natural);
+}
+
+template <typename T>
+void launch_combine(long n, int mode, double ds, const cplx<T>* E, const cplx<T>* P1,
+                    const cplx<T>* P12, const cplx<T>* P2, const cplx<T>* vh,
+                    const cplx<T>* b1, const cplx<T>* b2, cplx<T>* out, cudaStream_t s) {
+  k_combine<T><<<grid_cap(n, 256), 256, 0, s>>>(n, mode, (T)ds, E, P1, P12, P2, vh, b1, b2, out);
+}
+
+template <typename T> void launch_convert(long n, const double* in, T* out, cudaStream_t s) {
+  k_convert<T><<<grid_cap(n, 256), 256, 0, s>>>(n, in, out);
+}
+
+#define NWB_INST(T)                                                                            \
+  template void launch_theta_c2r<T>(const ThetaArgs<T>&, int, cudaStream_t);                   \
+  template void launch_theta_r2c<T>(const ThetaArgs<T>&, int, cudaStream_t);                   \
+  template void launch_rho<T>(const RhoArgs<T>&, int, int, cudaStream_t);                      \
+  template void launch_transpose<T>(const Geom&, const cplx<T>*, cplx<T>*, int, cudaStream_t); \
+  template void launch_combine<T>(long, int, double, const cplx<T>*, const cplx<T>*,           \
+                                  const cplx<T>*, const cplx<T>*, const cplx<T>*,              \
+                                  const cplx<T>*, const cplx<T>*, cplx<T>*, cudaStream_t);     \
+  template void launch_convert<T>(long, const double*, T*, cudaStream_t);
+NWB_INST(double)
+NWB_INST(float)
+
+}  // namespace nwb
