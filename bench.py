@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""Benchmark of the ExpRK22/WENO5 sigma-step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c2|c1|c3|c4|c5] [--no-e2e] [--no-cpu] [--no-fp32]
+
+Workload (N = 1): BASELINE config C2 = the paper's full-size grid, Set 4
+(N_rho = 10000, N_theta = 3584, Sigma = 120, N_sigma = 2400, homogeneous air)
+with the rho-modulated N-wave; synthetic inputs, fp64 headline
+and fp32 beside it.  One step = one full ExpRK22 sigma-step (4 transforms,
+2 WENO evaluations, 2 spectral combines) on the whole grid; the metric is
+grid-cell updates per second (cells x steps / s).
+
+For N > 1 (torchrun, one rank per GPU) every rank marches an independent
+member of an ensemble (BASELINE C4's sharding: no collective on the data
+path), so per-GPU work is fixed -> "scaling": "weak".  Timing: W warm-up
+steps, then exactly K steps between barrier + synchronize, CUDA events on
+the plan's stream, max over ranks.  The working set (>= 3 GB at C2) exceeds
+the 126 MB L2, so no flush is needed between steps.
+
+``--impl reference`` times the reference algorithm's CPU implementation on
+this host (the oracle port in oracle/: the reference's own WENO arithmetic
+in C + scipy's pocketfft, all host threads) on the same config; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid-cell updates/s per KZK ExpRK22 step"
+UNIT = "cell-steps/s"
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+FALLBACK_HBM_GBS = 6650.0
+
+
+# ------------------------------------------------------------------ workload
+
+def workload(name: str):
+    import paper_2103_06080_b200 as nw
+
+    if name == "c1":
+        cfg = nw.DomainConfig(Sigma=30.0, N_sigma=300, N_rho=625, N_theta=448)
+        desc = "C1 demo grid 625x448 homogeneous N-wave"
+    elif name == "c3":
+        cfg = nw.preset_config(1)
+        desc = "C3 Set-1 1250x448 turbulent (seed 0) N-wave"
+    elif name == "c5":
+        cfg = nw.DomainConfig(Sigma=120.0, N_sigma=6000, N_rho=8192, N_theta=16384)
+        desc = "C5 large grid 8192x16384 homogeneous rho-modulated N-wave"
+    else:
+        cfg = nw.preset_config(4)
+        desc = "C2 paper Set 4 10000x3584 homogeneous air, rho-modulated N-wave"
+    return cfg, desc
+
+
+def initial_field(cfg, rank: int = 0):
+    import paper_2103_06080_b200 as nw
+
+    _, rho, theta = nw.build_axes(cfg)
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B))
+    return v0.values * (1.0 - 0.02 * rank)
+
+
+def coefficient_fields(cfg, name: str, rows: int):
+    import paper_2103_06080_b200 as nw
+
+    rows = min(rows, cfg.N_sigma + 1)
+    if name == "c3":
+        sig, _, _ = nw.build_axes(cfg)
+        spec = nw.sample_modes(nw.TurbulenceParams(seed=0))
+        return nw.evaluate_fields(spec, spec.lam, sig[:rows], nw.rho_nodes_closed(cfg))
+    return nw.zero_fields(rows, cfg.N_rho + 1)
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while running."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, index: int, period: float = 0.02):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                ids = [x for x in vis.split(",") if x.strip()]
+                ent = ids[index].strip() if index < len(ids) else str(index)
+                h = (pynvml.nvmlDeviceGetHandleByUUID(ent) if not ent.isdigit()
+                     else pynvml.nvmlDeviceGetHandleByIndex(int(ent)))
+            else:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nvml, self.h = pynvml, h
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:
+            pass
+        self.period = period
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _reasons(self):
+        n = self.nvml
+        fn = getattr(n, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(n, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        return fn(self.h)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                bits = self._reasons()
+                for b, name in self.REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml-unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ roofline
+
+KERNELS = ("theta_c2r", "weno", "theta_r2c", "rho_stage1", "theta_c2r", "weno", "theta_r2c",
+           "rho_stage2")
+
+
+def algorithmic_bytes(cfg, precision: str):
+    """Compulsory HBM bytes per launch of each kernel slot."""
+    r = 8 if precision == "double" else 4
+    phys = cfg.N_rho * cfg.N_theta * r
+    spec = cfg.N_rho * (cfg.N_theta // 2 + 1) * 2 * r
+    c2r = spec + phys
+    weno = 2 * phys
+    r2c = phys + spec
+    rho1 = 7 * spec   # read b~, Vh, E, Phi1, Phi1m2; write U, T*
+    rho2 = 5 * spec   # read b~, U, Phi2; write Vh, T
+    return [c2r, weno, r2c, rho1, c2r, weno, r2c, rho2]
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic(config: str, precision: str, kernel: str):
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            t = json.load(fh)
+        return t[config][precision][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof):
+    abytes = algorithmic_bytes(cfg, precision)
+    peak, kind = hbm_peak()
+    per = []
+    for i, name in enumerate(KERNELS):
+        ms = kernel_ms_total[i] / n_prof
+        if ms <= 0:
+            continue
+        per.append({"slot": i, "kernel": name, "ms": round(ms, 5), "bytes": abytes[i],
+                    "GBs": round(abytes[i] / (ms * 1e-3) / 1e9, 1)})
+    # dominant kernel type by summed time over the step
+    by_kernel = {}
+    for p in per:
+        d = by_kernel.setdefault(p["kernel"], {"ms": 0.0, "bytes": 0, "n": 0})
+        d["ms"] += p["ms"]; d["bytes"] += p["bytes"]; d["n"] += 1
+    step_ms = sum(p["ms"] for p in per)
+    dom = max(by_kernel, key=lambda k: by_kernel[k]["ms"])
+    d = by_kernel[dom]
+    achieved = d["bytes"] / d["n"] / (d["ms"] / d["n"] * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+            "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "traffic": ncu_traffic(cname, precision, dom),
+            "share_of_step": round(d["ms"] / step_ms, 4),
+            "per_kernel": per}
+
+
+# ------------------------------------------------------------------ arms
+
+def dist_setup():
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def time_precision(cfg, cname, precision, steps, warmup, world, rank, local, clocks=True):
+    import torch
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    eps = 2.0 ** -53 if precision == "double" else 2.0 ** -24
+    n_prof = max(2, min(steps, 10))
+    rows = warmup + steps + n_prof + 2
+    fields = coefficient_fields(cfg, cname, rows)
+    plan = DevicePlan(cfg.N_rho, cfg.N_theta, 1, precision, cfg.d_sigma, cfg.rho_span,
+                      cfg.theta_span, cfg.A, cfg.B, eps, torch.device("cuda", local))
+    plan.set_coeffs(fields.u_par, fields.u_perp, fields.du_perp_drho,
+                    n_rows=fields.u_par.shape[0])
+    plan.load_physical(initial_field(cfg, rank))
+    plan.march("exprk22", 0, warmup, timing=False)
+    torch.cuda.synchronize(local)
+    barrier(world)
+    torch.cuda.synchronize(local)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        start.record(plan.stream)
+        max_abs, _, _ = plan.march("exprk22", warmup, steps, timing=False)
+        end.record(plan.stream)
+        torch.cuda.synchronize(local)
+    barrier(world)
+    ms = start.elapsed_time(end)
+    ms_max = max_over_ranks(ms, world)
+    kernel_ms = plan.profile_kernels("exprk22", warmup + steps, n_prof)
+    cells = cfg.N_rho * cfg.N_theta
+    res = {
+        "value": world * cells * steps / (ms_max * 1e-3),
+        "ms_per_step": ms_max / steps,
+        "roofline": roofline_block(cfg, cname, precision, kernel_ms, n_prof),
+        "max_abs_v_last": float(max_abs[0, -1]),
+        "clocks": sampler.summary() if clocks else None,
+        "plan_bytes": plan.bytes,
+    }
+    plan.close()
+    return res
+
+
+def e2e_precision(cfg, cname, precision, steps, world, rank, local):
+    """Same metric through the public API with host buffers (run_exprk22)."""
+    import torch
+    import paper_2103_06080_b200 as nw
+
+    v0 = initial_field(cfg, rank)
+    fields = coefficient_fields(cfg, cname, steps + 1)
+    torch.cuda.synchronize(local)
+    barrier(world)
+    t0 = time.perf_counter()
+    rep = nw.run_exprk22(cfg, nw.Field2D(v0), fields, precision=precision, max_steps=steps,
+                         timing=False, device=torch.device("cuda", local))
+    final = rep.final.values
+    wall = time.perf_counter() - t0
+    wall_max = max_over_ranks(wall, world)
+    r = 8 if precision == "double" else 4
+    h2d = v0.size * 8 + 3 * (steps + 1) * cfg.N_rho * 8
+    d2h = final.size * 8 + 8 * steps
+    return {"value": world * cfg.N_rho * cfg.N_theta * steps / wall_max, "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d / steps), "d2h_bytes_per_step": int(d2h / steps),
+            "wall_s": wall_max, "steps": steps,
+            "note": "run_exprk22(numpy v0, numpy fields) incl. plan build, H2D, D2H of the "
+                    f"float64 final field; working precision {r * 8}-bit"}
+
+
+def cpu_reference(cfg, cname, steps_cap=3, warm=1, threads=0, precision="double"):
+    """The reference algorithm on the host cores (oracle port)."""
+    from oracle import nwave_oracle as oracle
+
+    oracle.build()
+    cores = threads if threads > 0 else oracle.host_cores()
+    n = warm + steps_cap
+    fields = coefficient_fields(cfg, cname, n + 1)
+    v0 = initial_field(cfg)
+    run = oracle.march(cfg, v0, fields, precision=precision, threads=cores, max_steps=n)
+    secs = run.step_seconds[warm:]
+    med = float(np.median(secs))
+    return {"value": cfg.N_rho * cfg.N_theta / med, "unit": UNIT, "cores": cores,
+            "kind": "port", "s_per_step": med,
+            "sample": f"{steps_cap} timed ExpRK22 steps after {warm} warm-up on {cname} "
+                      f"({precision}), median; oracle/ port = reference WENO5 arithmetic "
+                      "in C (OpenMP) + scipy pocketfft (workers=cores) + numpy combines"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
+    args = ap.parse_args()
+    warmup = max(args.warmup, 3)
+    cfg, desc = workload(args.config)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    config = {"workload": desc, "n_rho": cfg.N_rho, "n_theta": cfg.N_theta,
+              "cells": cfg.N_rho * cfg.N_theta, "sigma_steps_full_run": cfg.N_sigma,
+              "scheme": "exprk22",
+              "l2": "working set > 3 GB >> 126 MB L2 (no flush needed)" if args.config in ("c2", "c5")
+              else "working set partly L2-resident",
+              "parallelism": f"ensemble-shard x{args.gpus}" if args.gpus > 1 else "single grid, 1 GPU"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = min(args.steps, 3)
+        cpu = cpu_reference(cfg, args.config, steps_cap=steps, warm=1)
+        line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus,
+                "steps": steps, "warmup": 1, "ms_per_step": cpu["s_per_step"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": config, "impl": "reference",
+                "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    world, rank, local = dist_setup()
+    res64 = time_precision(cfg, args.config, "double", args.steps, warmup, world, rank, local)
+    res32 = None
+    if not args.no_fp32:
+        res32 = time_precision(cfg, args.config, "single", args.steps, warmup, world, rank, local)
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_precision(cfg, args.config, "double", args.steps, world, rank, local)
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        cpu = cpu_reference(cfg, args.config)
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": res64["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": warmup, "ms_per_step": res64["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config,
+        "e2e": e2e, "gpu_launches": 8 * args.steps,
+        "roofline": res64["roofline"],
+        "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                         if cpu else None),
+        "clocks": res64["clocks"],
+        "fp32": ({"value": res32["value"], "ms_per_step": res32["ms_per_step"],
+                  "roofline": res32["roofline"], "clocks": res32["clocks"]} if res32 else None),
+        "impl": "b200",
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -111,6 +111,12 @@ int nwb_march(nwb_plan* plan, int scheme, int n0, int n_steps, double guard,
 /* One step from absolute step n without guard bookkeeping (graph-free). */
 int nwb_step(nwb_plan* plan, int scheme, int n);
 
+/* Measurement hook: march n_steps more steps from n0 with a CUDA event
+ * around every kernel and return the summed device ms per kernel slot:
+ * kernel_ms[8] = stage-1 (c2r, weno, r2c, rho), stage-2 (c2r, weno, r2c, rho).
+ * Requires a prior nwb_march covering [n0, n0 + n_steps). */
+int nwb_profile_kernels(nwb_plan* plan, int scheme, int n0, int n_steps, float* kernel_ms);
+
 /* SpectralTransforms: rfft2 (batch, n_rho, n_theta) real -> natural half
  * spectrum; irfft2 the inverse (Im of the theta DC / Nyquist bins dropped,
  * scaled 1/(n_rho n_theta)). */

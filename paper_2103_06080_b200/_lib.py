@@ -34,7 +34,7 @@ ABI_SYMBOLS = (
     "nwb_plan_destroy", "nwb_plan_set_stream", "nwb_plan_bytes", "nwb_plan_set_coeffs",
     "nwb_plan_load_physical", "nwb_plan_load_spectrum", "nwb_plan_store_spectrum",
     "nwb_plan_store_physical", "nwb_march", "nwb_step", "nwb_rfft2", "nwb_irfft2",
-    "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine",
+    "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine", "nwb_profile_kernels",
 )
 
 _lock = threading.Lock()
@@ -65,6 +65,7 @@ def _declare(lib):
                               c_int, c_void_p, c_void_p, c_void_p, P(c_int), P(c_int),
                               P(c_double)]),
         "nwb_step": (c_int, [c_void_p, c_int, c_int]),
+        "nwb_profile_kernels": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p]),
         "nwb_rfft2": (c_int, [c_void_p, c_void_p, c_void_p]),
         "nwb_irfft2": (c_int, [c_void_p, c_void_p, c_void_p]),
         "nwb_weno5_b": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,

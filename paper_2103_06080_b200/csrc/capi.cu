@@ -192,9 +192,13 @@ template <typename T> WenoArgs<T> weno_args(const nwb_plan* p) {
 }
 
 // One stage of the fused pipeline: c2r(+alpha, +vmax) -> WENO -> r2c -> rho pass.
+// ev (optional) holds 5 events: before c2r and after each of the 4 kernels.
+constexpr int EV_PER_STAGE = 5;
+
 template <typename T>
 void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   cudaStream_t s = p->stream;
+  if (ev) cudaEventRecord(ev[0], s);
   // theta c2r of T (stage 1) or T* (stage 2) into v
   ThetaArgs<T> c = theta_args<T>(p);
   c.spec_in = (const cplx<T>*)(stage == 1 ? p->t : p->ts);
@@ -205,19 +209,20 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   c.alpha_bits = p->red + (stage - 1);
   c.vmax_bits = stage == 1 ? p->vmax_hist : nullptr;
   launch_theta_c2r<T>(c, p->theta_rows, s);
-  if (ev) cudaEventRecord(ev[0], s);
+  if (ev) cudaEventRecord(ev[1], s);
   // WENO -> b
   WenoArgs<T> w = weno_args<T>(p);
   w.step_ctr = p->step_ctr;
   w.row_off = stage - 1;
   w.alpha_bits = p->red + (stage - 1);
   launch_weno<T>(w, s);
+  if (ev) cudaEventRecord(ev[2], s);
   // theta r2c of b -> bt
   ThetaArgs<T> r = theta_args<T>(p);
   r.phys_in = (const T*)p->b;
   r.spec_out = (cplx<T>*)p->bt;
   launch_theta_r2c<T>(r, p->theta_rows, s);
-  if (ev) cudaEventRecord(ev[1], s);
+  if (ev) cudaEventRecord(ev[3], s);
   // rho pass
   RhoArgs<T> q = rho_args<T>(p);
   q.in = (const cplx<T>*)p->bt;
@@ -238,13 +243,33 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
     q.zero_bits = p->red + 0;
   }
   launch_rho<T>(q, mode, p->rho_threads, s);
+  if (ev) cudaEventRecord(ev[4], s);
 }
 
+// ev (optional): 2 * EV_PER_STAGE events
 template <typename T> void launch_step(nwb_plan* p, int scheme, cudaEvent_t* ev) {
-  if (ev) cudaEventRecord(ev[0], p->stream);
-  launch_stage<T>(p, 1, scheme, ev ? ev + 1 : nullptr);
-  if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev ? ev + 3 : nullptr);
-  if (ev) cudaEventRecord(ev[5], p->stream);
+  launch_stage<T>(p, 1, scheme, ev);
+  if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev ? ev + EV_PER_STAGE : nullptr);
+}
+
+// per-step guard history [batch][len]; reallocation invalidates captured graphs
+int ensure_hist(nwb_plan* p, int len) {
+  if (p->hist_len >= len && p->vmax_hist) return NWB_OK;
+  if (p->vmax_hist) {
+    cudaFree(p->vmax_hist);
+    for (auto& x : p->allocs)
+      if (x == p->vmax_hist) x = nullptr;
+  }
+  p->vmax_hist = nullptr;
+  p->hist_len = len;
+  TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)p->g.batch * len * sizeof(u64)));
+  CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)p->g.batch * len * sizeof(u64), p->stream));
+  for (int i = 0; i < 2; ++i)
+    if (p->graph[i]) {
+      cudaGraphExecDestroy(p->graph[i]);
+      p->graph[i] = nullptr;
+    }
+  return NWB_OK;
 }
 
 int set_step(nwb_plan* p, int n) {
@@ -341,6 +366,12 @@ template <typename T> int set_coeffs_impl(nwb_plan* p, const double* up, const d
   TRY(dalloc(p, &p->du, n * sizeof(T)));
   TRY(dalloc(p, (void**)&p->alpha_rho, (size_t)n_rows * sizeof(double)));
   p->n_rows = n_rows;
+  for (int i = 0; i < 2; ++i)  // captured steps point at the old coefficient buffers
+    if (p->graph[i]) {
+      cudaGraphExecDestroy(p->graph[i]);
+      p->graph[i] = nullptr;
+    }
+  TRY(ensure_hist(p, n_rows));
   double* stage = nullptr;
   CU(cudaMalloc(&stage, n * sizeof(double)));
   const double* srcs[3] = {up, uq, du};
@@ -511,22 +542,7 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
   if (need_rows > p->n_rows)
     return fail(NWB_EINVAL, "coefficient rows do not cover the march (" + std::to_string(need_rows) +
                                 " > " + std::to_string(p->n_rows) + ")");
-  // per-step guard history
-  if (p->hist_len < n0 + n_steps) {
-    if (p->vmax_hist) {
-      cudaFree(p->vmax_hist);
-      for (auto& x : p->allocs)
-        if (x == p->vmax_hist) x = nullptr;
-    }
-    p->vmax_hist = nullptr;
-    p->hist_len = n0 + n_steps;
-    TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)g.batch * p->hist_len * sizeof(u64)));
-    for (int i = 0; i < 2; ++i)
-      if (p->graph[i]) {
-        cudaGraphExecDestroy(p->graph[i]);
-        p->graph[i] = nullptr;
-      }
-  }
+  TRY(ensure_hist(p, n0 + n_steps));
   CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)g.batch * p->hist_len * sizeof(u64), p->stream));
   CU(cudaMemsetAsync(p->red, 0, (size_t)g.batch * 4 * sizeof(u64), p->stream));
   TRY(set_step(p, n0));
@@ -535,7 +551,7 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
 
   std::vector<cudaEvent_t> evs;
   if (step_ms) {
-    evs.resize((size_t)n_steps * 6);
+    evs.resize((size_t)n_steps * 2 * EV_PER_STAGE);
     for (auto& e : evs) CU(cudaEventCreate(&e));
   }
   auto destroy_events = [&]() {
@@ -555,14 +571,12 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
       for (int q = 0; q < n_snap; ++q)
         if (snap_steps[q] == n) snap = q;
       if (step_ms) {
-        cudaEvent_t* ev = &evs[(size_t)(done + i) * 6];
-        cudaEventRecord(ev[0], p->stream);
-        launch_stage<T>(p, 1, scheme, ev + 1);
+        cudaEvent_t* ev = &evs[(size_t)(done + i) * 2 * EV_PER_STAGE];
+        launch_stage<T>(p, 1, scheme, ev);
         if (snap >= 0)
           cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
                           cudaMemcpyDeviceToDevice, p->stream);
-        if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev + 3);
-        cudaEventRecord(ev[5], p->stream);
+        if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev + EV_PER_STAGE);
       } else if (snap >= 0) {
         launch_stage<T>(p, 1, scheme, nullptr);
         cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
@@ -617,12 +631,12 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
   if (step_ms) {
     const int ran = done;
     for (int i = 0; i < ran; ++i) {
-      cudaEvent_t* ev = &evs[(size_t)i * 6];
-      float tot = 0, a = 0, b = 0, c = 0, d = 0;
-      cudaEventElapsedTime(&tot, ev[0], ev[5]);
-      cudaEventElapsedTime(&a, ev[1], ev[2]);  // WENO + r2c, stage 1
-      if (scheme == NWB_SCHEME_EXPRK22) cudaEventElapsedTime(&b, ev[3], ev[4]);
-      (void)c; (void)d;
+      cudaEvent_t* ev = &evs[(size_t)i * 2 * EV_PER_STAGE];
+      const bool two = scheme == NWB_SCHEME_EXPRK22;
+      float tot = 0, a = 0, b = 0;
+      cudaEventElapsedTime(&tot, ev[0], ev[two ? 2 * EV_PER_STAGE - 1 : EV_PER_STAGE - 1]);
+      cudaEventElapsedTime(&a, ev[1], ev[3]);  // WENO + theta r2c, stage 1
+      if (two) cudaEventElapsedTime(&b, ev[EV_PER_STAGE + 1], ev[EV_PER_STAGE + 3]);
       step_ms[(size_t)i * 3 + 0] = tot;
       step_ms[(size_t)i * 3 + 1] = a + b;
       step_ms[(size_t)i * 3 + 2] = tot - (a + b);
@@ -632,9 +646,45 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
   return rc;
 }
 
+// Per-kernel device time over n_steps steps (events around every launch):
+// kernel_ms[s*4 + i] for stage s in {0,1}, kernel i in (c2r, weno, r2c, rho).
+template <typename T>
+int profile_impl(nwb_plan* p, int scheme, int n0, int n_steps, float* kernel_ms) {
+  if (!p->upar) return fail(NWB_EINVAL, "coefficients not set (nwb_plan_set_coeffs)");
+  if (n0 + n_steps + 1 > p->n_rows) return fail(NWB_EINVAL, "coefficient rows do not cover the run");
+  if (p->hist_len < n0 + n_steps) return fail(NWB_EINVAL, "run nwb_march over this range first");
+  TRY(set_step(p, n0));
+  std::vector<cudaEvent_t> evs((size_t)n_steps * 2 * EV_PER_STAGE);
+  for (auto& e : evs) CU(cudaEventCreate(&e));
+  for (int i = 0; i < n_steps; ++i) launch_step<T>(p, scheme, &evs[(size_t)i * 2 * EV_PER_STAGE]);
+  cudaError_t e = cudaStreamSynchronize(p->stream);
+  for (int k = 0; k < 8; ++k) kernel_ms[k] = 0.f;
+  if (e == cudaSuccess) {
+    for (int i = 0; i < n_steps; ++i) {
+      cudaEvent_t* ev = &evs[(size_t)i * 2 * EV_PER_STAGE];
+      for (int st = 0; st < (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1); ++st)
+        for (int k = 0; k < 4; ++k) {
+          float ms = 0.f;
+          cudaEventElapsedTime(&ms, ev[st * EV_PER_STAGE + k], ev[st * EV_PER_STAGE + k + 1]);
+          kernel_ms[st * 4 + k] += ms;
+        }
+    }
+  }
+  for (auto& x : evs) cudaEventDestroy(x);
+  if (e != cudaSuccess) return fail(NWB_ECUDA, std::string("profile: ") + cudaGetErrorString(e));
+  return NWB_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
+
+int nwb_profile_kernels(nwb_plan* p, int scheme, int n0, int n_steps, float* kernel_ms) {
+  TRY(check_plan(p));
+  if (!kernel_ms || n_steps < 1) return fail(NWB_EINVAL, "bad profile arguments");
+  return p->prec == NWB_F64 ? profile_impl<double>(p, scheme, n0, n_steps, kernel_ms)
+                            : profile_impl<float>(p, scheme, n0, n_steps, kernel_ms);
+}
 
 extern "C" {
 
@@ -773,17 +823,7 @@ int nwb_step(nwb_plan* p, int scheme, int n) {
   TRY(check_plan(p));
   if (!p->upar) return fail(NWB_EINVAL, "coefficients not set");
   if (n + (scheme == NWB_SCHEME_EXPRK22 ? 1 : 0) >= p->n_rows) return fail(NWB_EINVAL, "coefficient rows do not cover the step");
-  if (p->hist_len < n + 1) {
-    if (p->vmax_hist) {
-      cudaFree(p->vmax_hist);
-      for (auto& x : p->allocs)
-        if (x == p->vmax_hist) x = nullptr;
-    }
-    p->vmax_hist = nullptr;
-    p->hist_len = n + 1;
-    TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)p->g.batch * p->hist_len * sizeof(u64)));
-    CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)p->g.batch * p->hist_len * sizeof(u64), p->stream));
-  }
+  TRY(ensure_hist(p, n + 1));
   TRY(set_step(p, n));
   return p->prec == NWB_F64 ? step_impl<double>(p, scheme, nullptr) : step_impl<float>(p, scheme, nullptr);
 }

@@ -210,6 +210,16 @@ class DevicePlan:
         check(rc, "nwb_march")
         return max_abs, step_ms, bufs
 
+    def profile_kernels(self, scheme: str, n0: int, n_steps: int) -> np.ndarray:
+        """Summed device ms per kernel slot over n_steps steps (CUDA events
+        around every launch): [c2r, weno, r2c, rho] x stage 1, stage 2."""
+        code = _lib.SCHEME_EXPRK22 if scheme == "exprk22" else _lib.SCHEME_EXPEULER
+        out = np.zeros(8, dtype=np.float32)
+        check(self.lib.nwb_profile_kernels(self._h, code, int(n0), int(n_steps),
+                                           out.ctypes.data_as(ctypes.c_void_p)),
+              "nwb_profile_kernels")
+        return out.astype(np.float64)
+
     def step(self, scheme: str, n: int):
         code = _lib.SCHEME_EXPRK22 if scheme == "exprk22" else _lib.SCHEME_EXPEULER
         check(self.lib.nwb_step(self._h, code, int(n)), "nwb_step")

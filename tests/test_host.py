@@ -1,0 +1,178 @@
+"""CPU (no GPU): host-side logic of the drop-in API and the C-ABI library
+(loads, exports every symbol include/nwb200.h declares; no compute calls)."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2103_06080_b200 as nw
+from paper_2103_06080_b200 import _lib
+from paper_2103_06080_b200.exprk import _snapshot_steps
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_builds_and_exports_every_header_symbol():
+    from paper_2103_06080_b200 import _build
+
+    _build.build()
+    lib = _lib.load_library()
+    with open(os.path.join(ROOT, "include", "nwb200.h")) as fh:
+        header = fh.read()
+    declared = set(re.findall(r"\b(nwb_[a-z0-9_]+)\s*\(", header))
+    assert declared == set(_lib.ABI_SYMBOLS)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert lib.nwb_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_2103_06080_b200 import _build
+
+    path = _build.build()
+    out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    with pytest.raises(nw.BackendError):
+        nw.weno5_b(np.zeros((4, 4)), np.zeros(4), np.zeros(4), np.zeros(4), 0.05, 0.1, 0.1)
+    with pytest.raises(nw.BackendError):
+        nw.SpectralTransforms(8, 8).forward(np.zeros((8, 8)))
+    cfg = nw.DomainConfig(N_rho=8, N_theta=8, N_sigma=2)
+    with pytest.raises(nw.BackendError):
+        nw.run_exprk22(cfg, np.zeros((8, 8)), nw.zero_fields(3, 9))
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2103_06080_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                with open(os.path.join(dirpath, f)) as fh:
+                    src = fh.read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+def test_error_mapping():
+    assert issubclass(nw.ConfigError, ValueError)
+    assert issubclass(nw.InstabilityError, RuntimeError)
+    e = nw.InstabilityError(1.5, 12.0)
+    assert e.sigma == 1.5 and e.max_abs == 12.0 and "1.5" in str(e)
+    assert issubclass(nw.UnsupportedSizeError, ValueError)
+    assert issubclass(nw.UnsupportedSizeError, nw.BackendError)
+
+
+def test_domain_config_validation_and_spacings():
+    c = nw.DomainConfig()
+    assert c.N_rho == 1250 and c.N_theta == 448 and c.N_sigma == 300
+    assert c.d_sigma == 120.0 / 300
+    assert c.d_theta == pytest.approx(28 * np.pi / 448)
+    for bad in (dict(Sigma=0.0), dict(N_rho=0), dict(N_theta=2.5), dict(A=-1.0),
+                dict(rho_max=-1.0), dict(roi_rho=(0.0, 500.0)), dict(B=float("nan"))):
+        with pytest.raises(nw.ConfigError):
+            nw.DomainConfig(**bad)
+
+
+def test_field2d_and_norms():
+    f = nw.Field2D(np.arange(12, dtype=np.int64).reshape(3, 4))
+    assert f.values.dtype == np.float64 and f.n_rho == 3 and f.n_theta == 4
+    with pytest.raises(nw.ConfigError):
+        nw.Field2D(np.zeros(5))
+    g = nw.Field2D(np.ones((3, 4)))
+    assert nw.l2_norm(g, 0.5, 2.0) == pytest.approx(np.sqrt(12.0))
+    assert nw.relative_error(g, g, 1.0, 1.0) == 0.0
+    with pytest.raises(ValueError):
+        nw.relative_error(nw.Field2D(np.zeros((3, 4))), g, 1.0, 1.0)
+    with pytest.raises(ValueError):
+        nw.l2_norm(nw.Field2D(np.full((2, 2), np.nan)), 1.0, 1.0)
+    assert nw.max_relative(np.array([1.0, -2.0]), np.array([1.0, -2.5])) == 0.25
+
+
+def test_axes_and_region():
+    c = nw.DomainConfig(N_rho=10, N_theta=8, N_sigma=4, Sigma=2.0)
+    s, r, t = nw.build_axes(c)
+    assert len(s) == 5 and len(r) == 10 and len(t) == 8
+    assert s[-1] == pytest.approx(2.0)
+    assert len(nw.rho_nodes_closed(c)) == 11
+    sub, rr, tt = nw.extract_region(nw.Field2D(np.ones((10, 8))), r, t, (40.0, 120.0),
+                                    (0.0, 15 * np.pi))
+    assert sub.n_rho == len(rr) and rr[0] >= 40.0 - 1e-9 and rr[-1] <= 120.0 + 1e-9
+
+
+def test_snapshot_plan_rounds_like_reference():
+    c = nw.DomainConfig(N_sigma=300)
+    plan = _snapshot_steps(c, [0.0, 60.0, 120.0, 130.0, 0.39])
+    assert plan == {0: 0.0, 150: 60.0, 300: 120.0, 1: 0.39}
+    assert _snapshot_steps(c, None) == {}
+
+
+def test_initial_nwave_and_ensemble_members():
+    c = nw.preset_config(1)
+    _, rho, theta = nw.build_axes(c)
+    v0 = nw.initial_nwave(rho, theta, c.A, c.B)
+    assert v0.values.shape == (1250, 448)
+    assert np.max(np.abs(v0.values)) == pytest.approx(0.9375, abs=1e-3)
+    with pytest.raises(ValueError):
+        nw.initial_nwave(rho, theta, 0.0)
+    members, amp, dur = nw.ensemble_nwaves(c, 8, seed=2026)
+    assert members.shape == (8, 1250, 448)
+    assert np.all((amp >= 0.5) & (amp <= 1.5)) and np.all((dur >= 0.75) & (dur <= 1.25))
+    again, _, _ = nw.ensemble_nwaves(c, 8, seed=2026)
+    assert np.array_equal(members, again)
+    # amplitude 1, duration 1 is the reference pulse up to rounding
+    row = nw.analysis._nwave_row(theta, c.B / (4 * c.A), 1.0, 1.0)
+    assert np.max(np.abs(row - v0.values[0])) <= 1e-12
+    # the pulse stays inside the periodic window
+    nz = np.nonzero(np.abs(members[:, 0]).max(axis=0) > 1e-8)[0]
+    assert theta[nz[0]] > 1.5 * np.pi and theta[nz[-1]] < 4.5 * np.pi
+
+
+def test_ground_metrics_interpolate_rise():
+    c = nw.DomainConfig(N_rho=10, N_theta=448)
+    _, _, theta = nw.build_axes(c)
+    # linear ramp of width pi starting at 2 pi (both corners on nodes, d_theta = pi/16)
+    y = np.clip((theta - 2 * np.pi) / np.pi, 0.0, 1.0)
+    f = nw.Field2D(np.tile(y, (10, 1)))
+    g = nw.ground_metrics(c, f, trace_rho=40.0)
+    assert g.peak == 1.0
+    assert g.rise_theta == pytest.approx(0.8 * np.pi, rel=1e-9)
+    assert g.rise_seconds == pytest.approx(g.rise_theta * 0.02 / (2 * np.pi))
+
+
+def test_cfl_report():
+    c = nw.preset_config(4)
+    rep = nw.check_cfl_exprk(c, nw.zero_fields(2, 10), 5.0)
+    assert rep.passed and rep.burgers_margin == pytest.approx(1.9635, rel=1e-4)
+    assert rep.transverse_margin == np.inf
+    bad = nw.check_cfl_splitting(nw.DomainConfig(N_sigma=2, Sigma=100.0))
+    assert not bad.passed and "FAIL" in str(bad)
+
+
+def test_downsample_fields():
+    f = nw.VelocityFields(*(np.arange(25.0).reshape(5, 5) for _ in range(4)))
+    d = nw.downsample_fields(f, 2, 1)
+    assert d.shape == (3, 5) and np.array_equal(d.u_par[1], f.u_par[2])
+    with pytest.raises(ValueError):
+        nw.downsample_fields(f, 3, 1)
+
+
+def test_bench_roofline_bookkeeping():
+    import bench
+
+    cfg, _ = bench.workload("c2")
+    b = bench.algorithmic_bytes(cfg, "double")
+    F = cfg.N_rho * cfg.N_theta * 8
+    spec = cfg.N_rho * (cfg.N_theta // 2 + 1) * 16
+    assert b[1] == 2 * F and b[3] == 7 * spec and b[7] == 5 * spec
+    blk = bench.roofline_block(cfg, "c2", "double", [1.0, 2.0, 1.0, 3.0, 1.0, 2.0, 1.0, 2.5], 1)
+    assert blk["kernel"] == "weno" and blk["unit"] == "GB/s"
+    assert 0 < blk["frac"] < 10
