@@ -38,40 +38,137 @@ int fail(int code, const std::string& msg) {
       return fail(NWB_ECUDA, std::string(what) + ": " + cudaGetErrorString(e_));       \
   } while (0)
 
-// radices for an n-point complex transform: 7s, 5s, 3s, then 8s and a 4 / 2
-bool factorize(int n, FftDesc& d) {
-  std::vector<int> r;
-  int m = n, twos = 0;
-  while (m % 2 == 0) { m /= 2; ++twos; }
-  for (int p : {7, 5, 3})
-    while (m % p == 0) { m /= p; r.push_back(p); }
+// ---------------------------------------------------------------- FFT plans
+// Stage radix sequence and its grouping into passes of one or two fused
+// stages (product <= 16 keeps a pass's elements in registers):
+// 7 pairs with 2, 5 with 3 or 2, 3 with 4 / 3 / 2, remaining powers of two
+// as 4x4 (16), 8, 4, 2.  split_two forces a lone radix-2 first stage (the
+// cluster-split rho pass performs it while loading).
+struct FftPlanHost {
+  std::vector<int> stages;              // radix per stage, DIF order
+  std::vector<std::pair<int, int>> passes;  // (ra, rb)
+};
+
+bool plan_fft(int n, bool split_two, FftPlanHost& h) {
+  int m = n, c2 = 0, c3 = 0, c5 = 0, c7 = 0;
+  while (m % 2 == 0) { m /= 2; ++c2; }
+  while (m % 3 == 0) { m /= 3; ++c3; }
+  while (m % 5 == 0) { m /= 5; ++c5; }
+  while (m % 7 == 0) { m /= 7; ++c7; }
   if (m != 1) return false;
-  while (twos >= 3) { r.push_back(8); twos -= 3; }
-  if (twos == 2) r.push_back(4);
-  if (twos == 1) r.push_back(2);
-  if ((int)r.size() > NWB_MAX_STAGES) return false;
-  d.n = n;
-  d.nst = (int)r.size();
-  int L = n;
-  for (int i = 0; i < d.nst; ++i) {
-    d.radix[i] = r[i];
-    d.span[i] = L;
-    L /= r[i];
+  std::vector<std::pair<int, int>> ps;
+  if (split_two) {
+    if (c2 == 0) return false;
+    ps.push_back({2, 1});
+    --c2;
+  }
+  for (; c7 > 0; --c7) {
+    if (c2 > 0) { ps.push_back({7, 2}); --c2; } else ps.push_back({7, 1});
+  }
+  for (; c5 > 0; --c5) {
+    if (c3 > 0) { ps.push_back({5, 3}); --c3; }
+    else if (c2 > 0) { ps.push_back({5, 2}); --c2; }
+    else ps.push_back({5, 1});
+  }
+  while (c3 > 0) {
+    if (c2 >= 2) { ps.push_back({3, 4}); c2 -= 2; --c3; }
+    else if (c3 >= 2) { ps.push_back({3, 3}); c3 -= 2; }
+    else if (c2 == 1) { ps.push_back({3, 2}); --c2; --c3; }
+    else { ps.push_back({3, 1}); --c3; }
+  }
+  // a leftover 8 / 4 / 2 goes first (after a forced split stage), so the last
+  // pass -- the one whose unit-stride butterflies set the smem padding -- is
+  // as large as possible
+  std::vector<std::pair<int, int>> head;
+  if (c2 % 4 == 3) head.push_back({8, 1});
+  if (c2 % 4 == 2) head.push_back({4, 1});
+  if (c2 % 4 == 1) head.push_back({2, 1});
+  ps.insert(ps.begin() + (split_two ? 1 : 0), head.begin(), head.end());
+  for (; c2 >= 4; c2 -= 4) ps.push_back({4, 4});
+  if ((int)ps.size() > NWB_MAX_PASSES) return false;
+  h.passes = ps;
+  h.stages.clear();
+  for (auto& q : ps) {
+    h.stages.push_back(q.first);
+    if (q.second > 1) h.stages.push_back(q.second);
   }
   return true;
 }
 
-// position after a DIF pass -> frequency
-std::vector<int> freq_of_pos(const FftDesc& d) {
-  std::vector<int> f(d.n);
-  for (int p = 0; p < d.n; ++p) {
-    int rem = p, ff = 0, mult = 1;
-    for (int s = 0; s < d.nst; ++s) {
-      const int span = d.span[s] / d.radix[s];
-      const int q = rem / span;
-      rem -= q * span;
+unsigned magic_for(int d) {
+  if (d <= 1) return 0u;
+  return (unsigned)((((unsigned long long)1 << 32) + (unsigned long long)d - 1) / (unsigned long long)d);
+}
+
+// device descriptor + per-stage twiddle tables W_L^{q i} laid out [q-1][i]
+template <typename T>
+void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& tw) {
+  const long double pi = 3.141592653589793238462643383279502884L;
+  std::vector<int> span, ofs;
+  tw.clear();
+  int L = n;
+  for (int r : h.stages) {
+    span.push_back(L);
+    ofs.push_back((int)tw.size());
+    const int s = L / r;
+    for (int q = 1; q < r; ++q)
+      for (int i = 0; i < s; ++i) {
+        // exact integer angle reduction: W_L^{q i} = W_n^{(q i mod L) n / L}
+        const long long t = (long long)q * i % L;
+        const long double a = 2.0L * pi * (long double)t / (long double)L;
+        cplx<T> w;
+        w.x = (T)cosl(a);
+        w.y = (T)-sinl(a);
+        tw.push_back(w);
+      }
+    L = s;
+  }
+  if (tw.empty()) tw.push_back(cplx<T>{1, 0});
+  std::memset(&d, 0, sizeof(d));
+  d.n = n;
+  d.np = (int)h.passes.size();
+  int st = 0;
+  for (int p = 0; p < d.np; ++p) {
+    const int ra = h.passes[p].first, rb = h.passes[p].second;
+    d.ptype[p] = 10 * ra + rb;
+    d.pspan[p] = span[st];
+    d.pofs_a[p] = ofs[st];
+    d.pofs_b[p] = rb > 1 ? ofs[st + 1] : 0;
+    const int sb = span[st] / ra / rb;
+    d.pmag_row[p] = magic_for(n / (ra * rb));
+    d.pmag_sb[p] = magic_for(sb);
+    st += rb > 1 ? 2 : 1;
+  }
+  // pad the smem line every P elements, P = size of the last pass, when P is
+  // even (an odd unit-stride pass is already bank-conflict free)
+  const int P = d.np ? (h.passes.back().first * h.passes.back().second) : 1;
+  d.pad_period = (P % 2 == 0 && P < n) ? P : 0;
+  if ((size_t)padded_len(n, d.pad_period) * sizeof(cplx<T>) > 227u * 1024u) d.pad_period = 0;
+  d.pad_magic = d.pad_period ? magic_for(d.pad_period) : 0u;
+  st = 0;
+  for (int p = 0; p < d.np; ++p) {
+    const int ra = h.passes[p].first, rb = h.passes[p].second;
+    const int sa = span[st] / ra, sb = sa / rb;
+    const int P2 = d.pad_period;
+    d.pfast[p] = P2 == 0 || sb % P2 == 0;
+    d.psa_p[p] = P2 ? sa + sa / P2 : sa;
+    d.psb_p[p] = P2 ? sb + sb / P2 : sb;
+    st += rb > 1 ? 2 : 1;
+  }
+}
+
+// position after a full DIF -> frequency
+std::vector<int> freq_of_pos(int n, const std::vector<int>& stages) {
+  std::vector<int> f(n);
+  for (int p = 0; p < n; ++p) {
+    int rem = p, ff = 0, mult = 1, L = n;
+    for (int r : stages) {
+      const int s = L / r;
+      const int q = rem / s;
+      rem -= q * s;
       ff += q * mult;
-      mult *= d.radix[s];
+      mult *= r;
+      L = s;
     }
     f[p] = ff;
   }
@@ -83,7 +180,6 @@ template <typename T> std::vector<cplx<T>> twiddles(int n, int count) {
   std::vector<cplx<T>> w(count);
   const long double pi = 3.141592653589793238462643383279502884L;
   for (int t = 0; t < count; ++t) {
-    // reduce to the first octant for accuracy: angle = 2 pi t / n
     const long double a = 2.0L * pi * (long double)t / (long double)n;
     w[t].x = (T)cosl(a);
     w[t].y = (T)-sinl(a);
@@ -101,6 +197,7 @@ struct nwb_plan {
   Geom g{};
   double d_sigma = 0, rho_span = 0, theta_span = 0, A = 0, B = 0, eps = 0;
   FftDesc dr{}, dh{};
+  FftPlanHost plan_r, plan_h;
   int theta_rows = 1, rho_threads = 256;
   size_t rsz = 8;  // sizeof(real)
   // device buffers
@@ -309,13 +406,14 @@ template <typename T> int create_impl(nwb_plan* p) {
   for (void* a : {p->vh, p->u, p->t, p->ts, p->bt}) CU(cudaMemsetAsync(a, 0, spec, p->stream));
 
   // twiddles and digit-reversal maps
-  auto twr = twiddles<T>(g.nr, g.nr);
-  auto twh = twiddles<T>(g.m, g.m);
+  std::vector<cplx<T>> twr, twh;
+  build_desc<T>(g.nr, p->plan_r, p->dr, twr);
+  build_desc<T>(g.m, p->plan_h, p->dh, twh);
   auto wk = twiddles<T>(g.nt, g.kk);
-  auto fr = freq_of_pos(p->dr);
+  auto fr = freq_of_pos(g.nr, p->plan_r.stages);
   std::vector<int> pr(g.nr);
   for (int q = 0; q < g.nr; ++q) pr[fr[q]] = q;
-  auto fh = freq_of_pos(p->dh);
+  auto fh = freq_of_pos(g.m, p->plan_h.stages);
   std::vector<int> ph(g.m);
   for (int q = 0; q < g.m; ++q) ph[fh[q]] = q;
   TRY(dalloc(p, &p->tw_r, twr.size() * C));
@@ -722,7 +820,7 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   p->A = A;
   p->B = B;
   p->eps = eps;
-  if (!factorize(n_rho, p->dr) || !factorize(p->g.m, p->dh)) {
+  if (!plan_fft(n_rho, false, p->plan_r) || !plan_fft(p->g.m, false, p->plan_h)) {
     delete p;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
   }

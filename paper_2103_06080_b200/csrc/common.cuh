@@ -48,4 +48,34 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v)
   return v;
 }
 
+// ---- asynchronous copies (sm_80+ LDGSTS, sm_90+ bulk L2 prefetch)
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// Prefetch [ptr, ptr + bytes) into L2 with one bulk (TMA) request per 64 KB;
+// bytes must be a multiple of 16 and ptr 16-byte aligned.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* ptr, unsigned bytes) {
+  const char* p = (const char*)ptr;
+  while (bytes) {
+    const unsigned chunk = bytes > 65536u ? 65536u : bytes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(chunk) : "memory");
+    p += chunk;
+    bytes -= chunk;
+  }
+}
+
+// complex loads/stores of 16-byte (double2) or 8-byte (float2) elements
+template <typename V> __device__ __forceinline__ void cp_async_c(V* dst, const V* src) {
+  if constexpr (sizeof(V) == 16) cp_async16(dst, src);
+  else cp_async8(dst, src);
+}
+
 }  // namespace nwb

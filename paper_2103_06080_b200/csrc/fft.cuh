@@ -23,14 +23,35 @@
 
 namespace nwb {
 
-#define NWB_MAX_STAGES 24
+#define NWB_MAX_PASSES 16
 
 struct FftDesc {
   int n;
-  int nst;
-  int radix[NWB_MAX_STAGES];
-  int span[NWB_MAX_STAGES];  // L of each stage (n, n/r1, n/(r1 r2), ...)
+  int np;                             // passes (1 or 2 fused stages each)
+  int ptype[NWB_MAX_PASSES];          // 10 * ra + rb (rb = 1: single stage)
+  int pspan[NWB_MAX_PASSES];          // L of the pass's first stage
+  int pofs_a[NWB_MAX_PASSES];         // twiddle-table offset, stage a
+  int pofs_b[NWB_MAX_PASSES];         // twiddle-table offset, stage b
+  unsigned pmag_row[NWB_MAX_PASSES];  // magic for x / (n / (ra rb)), 0 = divide by 1
+  unsigned pmag_sb[NWB_MAX_PASSES];   // magic for x / s_b
+  // bank-conflict padding of the shared-memory line: element e lives at
+  // e + e / pad_period (pad_period = element count of the last pass when it
+  // is even, so its unit-stride butterflies hit distinct banks); 0 = none
+  int pad_period;
+  unsigned pad_magic;
+  int pfast[NWB_MAX_PASSES];          // pad_period divides s_b: strides pre-padded
+  int psa_p[NWB_MAX_PASSES];          // padded s_a, s_b (valid when pfast)
+  int psb_p[NWB_MAX_PASSES];
 };
+
+// physical slot of logical element e in a (padded) shared-memory line
+__device__ __forceinline__ int pidx(const FftDesc& d, int e) {
+  return d.pad_period ? e + (int)__umulhi((unsigned)e, d.pad_magic) : e;
+}
+// padded line length for n logical elements
+__host__ __device__ inline int padded_len(int n, int pad_period) {
+  return pad_period ? n + n / pad_period + 1 : n + 1;  // one slot of slack (c2r stages X[n])
+}
 
 // ------------------------------------------------------------ butterflies
 // Forward uses w = exp(-2 pi i / r); INV uses the conjugate.
@@ -128,92 +149,174 @@ template <int RAD, bool INV, typename V> __device__ __forceinline__ void bfly(V*
   else bfly_odd<RAD, INV>(a);
 }
 
-// ------------------------------------------------------------ stages
-// `rows` independent transforms of length n at x + row*rstride.
+// ------------------------------------------------------------ passes
+// A pass is one stage or two consecutive stages (ra then rb) fused in
+// registers: a thread loads the ra*rb elements {base + m s_a + n s_b}, runs
+// rb stage-a butterflies and ra stage-b butterflies, and writes back -- one
+// shared-memory round trip for two stages.  Twiddles come from per-stage
+// tables tw[off + (q-1) s + i] = W_L^{q i} (coalesced over i; the stage
+// tables of one transform total n - 1 entries).  Index math uses
+// multiply-high magic numbers (exact for x * d < 2^32, checked on the host).
 
-template <int RAD, typename V>
-__device__ __forceinline__ void dif_stage(V* x, int n, int L, int rows, int rstride,
-                                          const V* __restrict__ tw) {
-  const int s = L / RAD;
-  const int per_row = n / RAD;
-  const int twm = n / L;
+template <bool CONJ, typename V> __device__ __forceinline__ V twmul(V a, V w) {
+  return CONJ ? cmulc(a, w) : cmul(a, w);
+}
+
+__device__ __forceinline__ unsigned fdiv(unsigned x, unsigned magic) {
+  return magic ? __umulhi(x, magic) : x;
+}
+
+// DIT=false: decimation in frequency (natural in, digit-reversed out);
+// DIT=true: decimation in time (digit-reversed in, natural out).  CONJ uses
+// conjugate roots and twiddles (unnormalised inverse transform).
+template <int RA, int RB, bool DIT, bool CONJ, typename V>
+__device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows, int rstride,
+                                         const V* __restrict__ tw) {
+  const int L = d.pspan[p];
+  const int sa = L / RA;            // stage-a span
+  const int sb = sa / RB;           // lane range
+  const int nb = d.n / L;           // blocks per row
+  const int per_row = nb * sb;
   const int total = per_row * rows;
+  const V* twa = tw + d.pofs_a[p];
+  const V* twb = tw + d.pofs_b[p];
   for (int g = threadIdx.x; g < total; g += blockDim.x) {
-    const int row = g / per_row;
+    const int row = (int)fdiv((unsigned)g, d.pmag_row[p]);
     const int h = g - row * per_row;
-    const int blk = h / s;
-    const int i = h - blk * s;
-    V* base = x + row * rstride + blk * L + i;
-    V a[RAD];
+    const int blk = (int)fdiv((unsigned)h, d.pmag_sb[p]);
+    const int i = h - blk * sb;
+    V* xr = x + row * rstride;
+    const int e0 = blk * L + i;
+    const bool fast = d.pfast[p];
+    const int pe0 = pidx(d, e0), psa = d.psa_p[p], psb = d.psb_p[p];
+    V a[RA * RB];
 #pragma unroll
-    for (int m = 0; m < RAD; ++m) a[m] = base[m * s];
-    bfly<RAD, false>(a);
-    if (i != 0) {
-      const int step = i * twm;
+    for (int m = 0; m < RA; ++m)
 #pragma unroll
-      for (int q = 1; q < RAD; ++q) a[q] = cmul(a[q], __ldg(tw + q * step));
+      for (int n2 = 0; n2 < RB; ++n2)
+        a[m * RB + n2] = xr[fast ? pe0 + m * psa + n2 * psb : pidx(d, e0 + m * sa + n2 * sb)];
+    if (!DIT) {
+      // stage a over m (lane i + n2 sb of span L), twiddle after
+#pragma unroll
+      for (int n2 = 0; n2 < RB; ++n2) {
+        V t[RA];
+#pragma unroll
+        for (int m = 0; m < RA; ++m) t[m] = a[m * RB + n2];
+        bfly<RA, CONJ>(t);
+        const int ia = i + n2 * sb;
+        if (ia != 0) {
+#pragma unroll
+          for (int q = 1; q < RA; ++q) t[q] = twmul<CONJ>(t[q], __ldg(twa + (q - 1) * sa + ia));
+        }
+#pragma unroll
+        for (int q = 0; q < RA; ++q) a[q * RB + n2] = t[q];
+      }
+      if (RB > 1) {
+        // stage b over n2 within each stage-a output q (lane i of span sa)
+#pragma unroll
+        for (int q = 0; q < RA; ++q) {
+          V t[RB];
+#pragma unroll
+          for (int n2 = 0; n2 < RB; ++n2) t[n2] = a[q * RB + n2];
+          bfly<RB, CONJ>(t);
+          if (i != 0) {
+#pragma unroll
+            for (int r = 1; r < RB; ++r) t[r] = twmul<CONJ>(t[r], __ldg(twb + (r - 1) * sb + i));
+          }
+#pragma unroll
+          for (int r = 0; r < RB; ++r) a[q * RB + r] = t[r];
+        }
+      }
+    } else {
+      // inverse: stage b first (DIT order), then stage a
+      if (RB > 1) {
+#pragma unroll
+        for (int q = 0; q < RA; ++q) {
+          V t[RB];
+#pragma unroll
+          for (int r = 0; r < RB; ++r) t[r] = a[q * RB + r];
+          if (i != 0) {
+#pragma unroll
+            for (int r = 1; r < RB; ++r) t[r] = twmul<CONJ>(t[r], __ldg(twb + (r - 1) * sb + i));
+          }
+          bfly<RB, CONJ>(t);
+#pragma unroll
+          for (int n2 = 0; n2 < RB; ++n2) a[q * RB + n2] = t[n2];
+        }
+      }
+#pragma unroll
+      for (int n2 = 0; n2 < RB; ++n2) {
+        V t[RA];
+#pragma unroll
+        for (int q = 0; q < RA; ++q) t[q] = a[q * RB + n2];
+        const int ia = i + n2 * sb;
+        if (ia != 0) {
+#pragma unroll
+          for (int q = 1; q < RA; ++q) t[q] = twmul<CONJ>(t[q], __ldg(twa + (q - 1) * sa + ia));
+        }
+        bfly<RA, CONJ>(t);
+#pragma unroll
+        for (int m = 0; m < RA; ++m) a[m * RB + n2] = t[m];
+      }
     }
 #pragma unroll
-    for (int q = 0; q < RAD; ++q) base[q * s] = a[q];
+    for (int m = 0; m < RA; ++m)
+#pragma unroll
+      for (int n2 = 0; n2 < RB; ++n2)
+        xr[fast ? pe0 + m * psa + n2 * psb : pidx(d, e0 + m * sa + n2 * sb)] = a[m * RB + n2];
   }
 }
 
-template <int RAD, typename V>
-__device__ __forceinline__ void dit_stage(V* x, int n, int L, int rows, int rstride,
-                                          const V* __restrict__ tw) {
-  const int s = L / RAD;
-  const int per_row = n / RAD;
-  const int twm = n / L;
-  const int total = per_row * rows;
-  for (int g = threadIdx.x; g < total; g += blockDim.x) {
-    const int row = g / per_row;
-    const int h = g - row * per_row;
-    const int blk = h / s;
-    const int i = h - blk * s;
-    V* base = x + row * rstride + blk * L + i;
-    V a[RAD];
-#pragma unroll
-    for (int q = 0; q < RAD; ++q) a[q] = base[q * s];
-    if (i != 0) {
-      const int step = i * twm;
-#pragma unroll
-      for (int q = 1; q < RAD; ++q) a[q] = cmulc(a[q], __ldg(tw + q * step));
-    }
-    bfly<RAD, true>(a);
-#pragma unroll
-    for (int m = 0; m < RAD; ++m) base[m * s] = a[m];
+// pass type codes (host planner in capi.cu): 10*ra + rb
+template <bool DIT, bool CONJ, typename V>
+__device__ __forceinline__ void run_pass(V* x, const FftDesc& d, int p, int rows, int rstride,
+                                         const V* tw) {
+  switch (d.ptype[p]) {
+    case 21: fft_pass<2, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 31: fft_pass<3, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 41: fft_pass<4, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 51: fft_pass<5, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 71: fft_pass<7, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 81: fft_pass<8, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 72: fft_pass<7, 2, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 53: fft_pass<5, 3, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 52: fft_pass<5, 2, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 34: fft_pass<3, 4, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 33: fft_pass<3, 3, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 32: fft_pass<3, 2, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    default: fft_pass<4, 4, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
   }
 }
 
-// Caller must __syncthreads() before (input staged); returns after a barrier.
+// All drivers expect the input staged (caller's __syncthreads()) and return
+// after a barrier.  first_pass > 0 skips leading passes (the cluster-split
+// rho pass performs the first radix-2 stage while loading).
+
+// forward DFT, natural -> digit-reversed
 template <typename V>
-__device__ void fft_forward(V* x, const FftDesc& d, int rows, int rstride, const V* tw) {
-  for (int st = 0; st < d.nst; ++st) {
-    const int L = d.span[st];
-    switch (d.radix[st]) {
-      case 2: dif_stage<2>(x, d.n, L, rows, rstride, tw); break;
-      case 3: dif_stage<3>(x, d.n, L, rows, rstride, tw); break;
-      case 4: dif_stage<4>(x, d.n, L, rows, rstride, tw); break;
-      case 5: dif_stage<5>(x, d.n, L, rows, rstride, tw); break;
-      case 7: dif_stage<7>(x, d.n, L, rows, rstride, tw); break;
-      default: dif_stage<8>(x, d.n, L, rows, rstride, tw); break;
-    }
+__device__ void fft_forward(V* x, const FftDesc& d, int rows, int rstride, const V* tw,
+                            int first_pass = 0) {
+  for (int p = first_pass; p < d.np; ++p) {
+    run_pass<false, false>(x, d, p, rows, rstride, tw);
     __syncthreads();
   }
 }
 
+// unnormalised inverse DFT, digit-reversed -> natural
 template <typename V>
-__device__ void fft_inverse(V* x, const FftDesc& d, int rows, int rstride, const V* tw) {
-  for (int st = d.nst - 1; st >= 0; --st) {
-    const int L = d.span[st];
-    switch (d.radix[st]) {
-      case 2: dit_stage<2>(x, d.n, L, rows, rstride, tw); break;
-      case 3: dit_stage<3>(x, d.n, L, rows, rstride, tw); break;
-      case 4: dit_stage<4>(x, d.n, L, rows, rstride, tw); break;
-      case 5: dit_stage<5>(x, d.n, L, rows, rstride, tw); break;
-      case 7: dit_stage<7>(x, d.n, L, rows, rstride, tw); break;
-      default: dit_stage<8>(x, d.n, L, rows, rstride, tw); break;
-    }
+__device__ void fft_inverse(V* x, const FftDesc& d, int rows, int rstride, const V* tw,
+                            int first_pass = 0) {
+  for (int p = d.np - 1; p >= first_pass; --p) {
+    run_pass<true, true>(x, d, p, rows, rstride, tw);
+    __syncthreads();
+  }
+}
+
+// unnormalised inverse DFT, natural -> digit-reversed
+template <typename V>
+__device__ void fft_inverse_dif(V* x, const FftDesc& d, int rows, int rstride, const V* tw) {
+  for (int p = 0; p < d.np; ++p) {
+    run_pass<false, true>(x, d, p, rows, rstride, tw);
     __syncthreads();
   }
 }

@@ -12,6 +12,9 @@
 // (batch, nr, nt) row-major; spectral arrays are (batch, kk, ld) with the
 // rho index contiguous, so the rho pass streams contiguous rows and the
 // theta passes move R-row segments (R x 16 B fp64) per theta mode.
+// Global -> shared staging uses cp.async (many 16-byte requests in flight
+// per thread); the rho pass prefetches its combine operands into L2 with
+// bulk (TMA) prefetches at entry so they arrive while the forward FFT runs.
 #include "internal.h"
 
 namespace nwb {
@@ -39,35 +42,49 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
   }
 }
 
+template <typename T> constexpr int theta_min_blocks() { return sizeof(T) == 8 ? 2 : 3; }
+
 // ------------------------------------------------------------------ theta c2r
-// X[0..m] (Im of X[0], X[m] dropped as pocketfft's c2r does) ->
+// X[0..m] staged in natural order (Im of X[0], X[m] dropped as pocketfft's c2r
+// does), then in place, pair by pair,
 //   Z[k] = (X[k] + conj X[m-k]) + i (X[k] - conj X[m-k]) conj(W_nt^k),  k < m
-// placed at digit-reversed slots, inverse m-point DIT, then
-//   v[2n] = Re z[n] * scale, v[2n+1] = Im z[n] * scale.
+//   Z[m-k] = conj(Ze) + i conj(Zo)
+// an inverse m-point DIF (natural in, digit-reversed out), and
+//   v[2n] = Re z[pos(n)] * scale, v[2n+1] = Im z[pos(n)] * scale.
 
 template <typename T, int R>
-__global__ void __launch_bounds__(256) k_theta_c2r(const ThetaArgs<T> a) {
+__global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
-  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
+  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld, kk = a.g.kk;
+  const int rs = padded_len(m, a.dh.pad_period);  // smem row stride (holds X[0..m])
   const int mem = blockIdx.y;
   const int j0 = blockIdx.x * R;
-  const V* src = a.spec_in + (size_t)mem * a.g.kk * ld;
+  const V* src = a.spec_in + (size_t)mem * kk * ld;
+  for (int idx = threadIdx.x; idx < kk * R; idx += blockDim.x) {
+    const int r = idx % R, k = idx / R, j = j0 + r;
+    V* slot = &z[r * rs + pidx(a.dh, k)];
+    if (j < nr) cp_async_c(slot, &src[(size_t)k * ld + j]);
+    else *slot = mk<V>(0, 0);
+  }
+  cp_async_wait_all();
+  __syncthreads();
   const int npairs = m / 2 + 1;
   for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
-    const int r = idx % R, k = idx / R, j = j0 + r;
-    if (j >= nr) continue;
-    V xk = src[(size_t)k * ld + j];
-    V xm = src[(size_t)(m - k) * ld + j];
+    const int r = idx / npairs, k = idx - r * npairs;
+    V* zr = z + r * rs;
+    const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
+    V xk = zr[sk];
+    V xm = zr[sm];
     if (k == 0) { xk.y = 0; xm.y = 0; }
     const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
     const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), a.wk[k]);
-    z[r * m + a.pos_h[k]] = mk<V>(ze.x - zo.y, ze.y + zo.x);
-    if (k != 0 && 2 * k != m) z[r * m + a.pos_h[m - k]] = mk<V>(ze.x + zo.y, zo.x - ze.y);
+    zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
+    if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
   }
   __syncthreads();
-  fft_inverse(z, a.dh, R, m, a.tw_h);
+  fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
 
   const int step = a.step_ctr ? *a.step_ctr : 0;
   const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * nr : nullptr;
@@ -77,7 +94,7 @@ __global__ void __launch_bounds__(256) k_theta_c2r(const ThetaArgs<T> a) {
   for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
     const int r = idx / m, n = idx - r * m, j = j0 + r;
     if (j >= nr) continue;
-    const V zz = z[r * m + n];
+    const V zz = z[r * rs + pidx(a.dh, a.pos_h[n])];
     const T v0 = zz.x * a.scale, v1 = zz.y * a.scale;
     *reinterpret_cast<V*>(dst + (size_t)j * a.g.nt + 2 * n) = mk<V>(v0, v1);
     const T c = up ? two_pi * up[j] : (T)0;
@@ -99,7 +116,7 @@ __global__ void __launch_bounds__(256) k_theta_c2r(const ThetaArgs<T> a) {
 //   X[k] = ze + W_nt^k zo,   X[m-k] = conj(ze - W_nt^k zo).
 
 template <typename T, int R>
-__global__ void __launch_bounds__(256) k_theta_r2c(const ThetaArgs<T> a) {
+__global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
@@ -107,21 +124,24 @@ __global__ void __launch_bounds__(256) k_theta_r2c(const ThetaArgs<T> a) {
   const int mem = blockIdx.y;
   const int j0 = blockIdx.x * R;
   const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
+  const int rs = padded_len(m, a.dh.pad_period);
   for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
     const int r = idx / m, n = idx - r * m, j = j0 + r;
-    z[idx] = j < nr ? *reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n)
-                    : mk<V>(0, 0);
+    V* slot = &z[r * rs + pidx(a.dh, n)];
+    if (j < nr) cp_async_c(slot, reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n));
+    else *slot = mk<V>(0, 0);
   }
+  cp_async_wait_all();
   __syncthreads();
-  fft_forward(z, a.dh, R, m, a.tw_h);
+  fft_forward(z, a.dh, R, rs, a.tw_h);
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
   for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
     if (j >= nr) continue;
-    const V zk = z[r * m + a.pos_h[k]];
-    const V zm = z[r * m + a.pos_h[k == 0 ? 0 : m - k]];
+    const V zk = z[r * rs + pidx(a.dh, a.pos_h[k])];
+    const V zm = z[r * rs + pidx(a.dh, a.pos_h[k == 0 ? 0 : m - k])];
     const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
     const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
     const V wz = cmul(a.wk[k], zo);
@@ -135,8 +155,12 @@ __global__ void __launch_bounds__(256) k_theta_r2c(const ThetaArgs<T> a) {
 
 // ------------------------------------------------------------------ rho pass
 
+template <typename V> __device__ __forceinline__ void prefetch_row(const V* p, int n) {
+  prefetch_l2_bulk(p, (unsigned)((size_t)n * sizeof(V)) & ~15u);
+}
+
 template <typename T, int MODE>
-__global__ void __launch_bounds__(1024) k_rho(const RhoArgs<T> a) {
+__global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* x = reinterpret_cast<V*>(smem_raw);
@@ -150,15 +174,33 @@ __global__ void __launch_bounds__(1024) k_rho(const RhoArgs<T> a) {
     for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = src[a.pos_r[f]];
     return;
   }
+  if (threadIdx.x == 0) {
+    // the combine operands are consumed after the forward FFT: start their
+    // DRAM -> L2 traffic now so it overlaps the transform
+    if (MODE == RHO_STAGE1) {
+      prefetch_row(a.vh + row, n);
+      prefetch_row(a.E + trow, n);
+      prefetch_row(a.P1 + trow, n);
+      prefetch_row(a.P12 + trow, n);
+    } else if (MODE == RHO_STAGE2) {
+      prefetch_row(a.u + row, n);
+      prefetch_row(a.P2 + trow, n);
+    } else if (MODE == RHO_EULER) {
+      prefetch_row(a.vh + row, n);
+      prefetch_row(a.E + trow, n);
+      prefetch_row(a.P1 + trow, n);
+    }
+  }
   if (MODE == RHO_INV_NAT) {
     for (int f = threadIdx.x; f < n; f += blockDim.x) {
       const int p = a.pos_r[f];
       const V val = src[f];
-      x[p] = val;
+      x[pidx(a.dr, p)] = val;
       if (a.vh) a.vh[row + p] = val;
     }
   } else {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) x[j] = src[j];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &src[j]);
+    cp_async_wait_all();
   }
   if (a.zero_bits && k == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
   __syncthreads();
@@ -166,28 +208,31 @@ __global__ void __launch_bounds__(1024) k_rho(const RhoArgs<T> a) {
 
   if (MODE == RHO_FWD_NAT) {
     V* dst = a.out + row;
-    for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = x[a.pos_r[f]];
+    for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = x[pidx(a.dr, a.pos_r[f])];
     return;
   }
   const T ds = a.ds;
+#pragma unroll 2
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    const V b = x[p];
+    const int sp = pidx(a.dr, p);
+    const V b = x[sp];
     if (MODE == RHO_STAGE1) {
-      const V ev = cmul(a.E[trow + p], a.vh[row + p]);
+      const V e = a.E[trow + p], vh = a.vh[row + p];
       const V p1 = a.P1[trow + p], p12 = a.P12[trow + p];
+      const V ev = cmul(e, vh);
       const V vs = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), b));
       a.u[row + p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), b));
-      x[p] = vs;
+      x[sp] = vs;
     } else if (MODE == RHO_STAGE2) {
-      const V p2 = a.P2[trow + p];
-      const V vn = cadd(a.u[row + p], cmul(mk<V>(ds * p2.x, ds * p2.y), b));
+      const V p2 = a.P2[trow + p], u = a.u[row + p];
+      const V vn = cadd(u, cmul(mk<V>(ds * p2.x, ds * p2.y), b));
       a.vh[row + p] = vn;
-      x[p] = vn;
+      x[sp] = vn;
     } else if (MODE == RHO_EULER) {
-      const V p1 = a.P1[trow + p];
-      const V vn = cadd(cmul(a.E[trow + p], a.vh[row + p]), cmul(mk<V>(ds * p1.x, ds * p1.y), b));
+      const V e = a.E[trow + p], vh = a.vh[row + p], p1 = a.P1[trow + p];
+      const V vn = cadd(cmul(e, vh), cmul(mk<V>(ds * p1.x, ds * p1.y), b));
       a.vh[row + p] = vn;
-      x[p] = vn;
+      x[sp] = vn;
     } else if (MODE == RHO_INIT) {
       a.vh[row + p] = b;
     }
@@ -195,7 +240,7 @@ __global__ void __launch_bounds__(1024) k_rho(const RhoArgs<T> a) {
   __syncthreads();
   fft_inverse(x, a.dr, 1, 0, a.tw_r);
   V* dst = a.out + row;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[j];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
 }
 
@@ -286,14 +331,14 @@ static inline int grid_cap(long n, int threads) {
 
 template <typename T, int R>
 static void c2r_r(const ThetaArgs<T>& a, cudaStream_t s) {
-  const size_t sm = (size_t)R * a.g.m * sizeof(cplx<T>);
+  const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_theta_c2r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
   k_theta_c2r<T, R><<<grid, 256, sm, s>>>(a);
 }
 template <typename T, int R>
 static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
-  const size_t sm = (size_t)R * a.g.m * sizeof(cplx<T>);
+  const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_theta_r2c<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
   k_theta_r2c<T, R><<<grid, 256, sm, s>>>(a);
@@ -318,7 +363,7 @@ template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cud
 
 template <typename T, int MODE>
 static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
-  const size_t sm = (size_t)a.dr.n * sizeof(cplx<T>);
+  const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid(a.g.batch, a.g.kk);
   k_rho<T, MODE><<<grid, threads, sm, s>>>(a);

@@ -161,6 +161,8 @@ def big():
         plan.march("exprk22", 44, 16, timing=False)
         torch.cuda.synchronize()
         out.append(("graph ms/step", (time.time() - t) / 16 * 1e3))
+        km = plan.profile_kernels("exprk22", 50, 8) / 8
+        out.append(("kernels ms [c2r weno r2c rho] x2", [round(float(x), 4) for x in km]))
         plan.close()
     return out
 
