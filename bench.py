@@ -59,10 +59,36 @@ def workload(name: str):
     elif name == "c5":
         cfg = nw.DomainConfig(Sigma=120.0, N_sigma=6000, N_rho=8192, N_theta=16384)
         desc = "C5 large grid 8192x16384 homogeneous rho-modulated N-wave"
+    elif name == "c4":
+        cfg = nw.preset_config(1)
+        desc = ("C4 ensemble of 256 Set-1 (1250x448) N-waves, amplitude U[0.5,1.5] x "
+                "duration U[0.75,1.25] (seed 2026), members sharded over ranks")
     else:
         cfg = nw.preset_config(4)
         desc = "C2 paper Set 4 10000x3584 homogeneous air, rho-modulated N-wave"
     return cfg, desc
+
+
+ENSEMBLE_MEMBERS = 256
+
+
+def members_for(cname: str, world: int, rank: int) -> range:
+    """Members this rank marches: the C4 shard, or one independent replica."""
+    from paper_2103_06080_b200.ensemble import shard_members
+
+    if cname == "c4":
+        return shard_members(ENSEMBLE_MEMBERS, world, rank)
+    return range(rank, rank + 1)
+
+
+def initial_fields(cfg, cname: str, members: range):
+    """(n, N_rho, N_theta) initial fields of the given members."""
+    import paper_2103_06080_b200 as nw
+
+    if cname == "c4":
+        all_v0, _, _ = nw.ensemble_nwaves(cfg, ENSEMBLE_MEMBERS, seed=2026)
+        return all_v0[members.start:members.stop]
+    return np.stack([initial_field(cfg, r) for r in members])
 
 
 def initial_field(cfg, rank: int = 0):
@@ -159,16 +185,22 @@ KERNELS = ("theta_c2r", "weno", "theta_r2c", "rho_stage1", "theta_c2r", "weno", 
            "rho_stage2")
 
 
-def algorithmic_bytes(cfg, precision: str):
-    """Compulsory HBM bytes per launch of each kernel slot."""
+def algorithmic_bytes(cfg, precision: str, batch: int = 1):
+    """Compulsory HBM bytes per launch of each kernel slot.
+
+    Per member: theta c2r / r2c and WENO move 1 field in + 1 out; the rho
+    passes stream b~ and the state (Vh, U) plus write two spectra; the
+    multiplier tables (E, Phi1, Phi1m2 in stage 1, Phi2 in stage 2) are read
+    once per launch and shared by all members of a batch.
+    """
     r = 8 if precision == "double" else 4
     phys = cfg.N_rho * cfg.N_theta * r
     spec = cfg.N_rho * (cfg.N_theta // 2 + 1) * 2 * r
-    c2r = spec + phys
-    weno = 2 * phys
-    r2c = phys + spec
-    rho1 = 7 * spec   # read b~, Vh, E, Phi1, Phi1m2; write U, T*
-    rho2 = 5 * spec   # read b~, U, Phi2; write Vh, T
+    c2r = batch * (spec + phys)
+    weno = batch * 2 * phys
+    r2c = batch * (phys + spec)
+    rho1 = batch * 4 * spec + 3 * spec   # read b~, Vh; write U, T*; tables E, Phi1, Phi1m2
+    rho2 = batch * 4 * spec + 1 * spec   # read b~, U; write Vh, T; table Phi2
     return [c2r, weno, r2c, rho1, c2r, weno, r2c, rho2]
 
 
@@ -189,8 +221,8 @@ def ncu_traffic(config: str, precision: str, kernel: str):
         return None
 
 
-def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof):
-    abytes = algorithmic_bytes(cfg, precision)
+def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
+    abytes = algorithmic_bytes(cfg, precision, batch)
     peak, kind = hbm_peak()
     per = []
     for i, name in enumerate(KERNELS):
@@ -259,11 +291,13 @@ def time_precision(cfg, cname, precision, steps, warmup, world, rank, local, clo
     n_prof = max(2, min(steps, 10))
     rows = warmup + steps + n_prof + 2
     fields = coefficient_fields(cfg, cname, rows)
-    plan = DevicePlan(cfg.N_rho, cfg.N_theta, 1, precision, cfg.d_sigma, cfg.rho_span,
-                      cfg.theta_span, cfg.A, cfg.B, eps, torch.device("cuda", local))
+    members = members_for(cname, world, rank)
+    plan = DevicePlan(cfg.N_rho, cfg.N_theta, len(members), precision, cfg.d_sigma,
+                      cfg.rho_span, cfg.theta_span, cfg.A, cfg.B, eps,
+                      torch.device("cuda", local))
     plan.set_coeffs(fields.u_par, fields.u_perp, fields.du_perp_drho,
                     n_rows=fields.u_par.shape[0])
-    plan.load_physical(initial_field(cfg, rank))
+    plan.load_physical(initial_fields(cfg, cname, members))
     plan.march("exprk22", 0, warmup, timing=False)
     torch.cuda.synchronize(local)
     barrier(world)
@@ -280,10 +314,11 @@ def time_precision(cfg, cname, precision, steps, warmup, world, rank, local, clo
     ms_max = max_over_ranks(ms, world)
     kernel_ms = plan.profile_kernels("exprk22", warmup + steps, n_prof)
     cells = cfg.N_rho * cfg.N_theta
+    total_members = ENSEMBLE_MEMBERS if cname == "c4" else world
     res = {
-        "value": world * cells * steps / (ms_max * 1e-3),
+        "value": total_members * cells * steps / (ms_max * 1e-3),
         "ms_per_step": ms_max / steps,
-        "roofline": roofline_block(cfg, cname, precision, kernel_ms, n_prof),
+        "roofline": roofline_block(cfg, cname, precision, kernel_ms, n_prof, len(members)),
         "max_abs_v_last": float(max_abs[0, -1]),
         "clocks": sampler.summary() if clocks else None,
         "plan_bytes": plan.bytes,
@@ -297,20 +332,29 @@ def e2e_precision(cfg, cname, precision, steps, world, rank, local):
     import torch
     import paper_2103_06080_b200 as nw
 
-    v0 = initial_field(cfg, rank)
+    members = members_for(cname, world, rank)
+    v0 = initial_fields(cfg, cname, members)
     fields = coefficient_fields(cfg, cname, steps + 1)
     torch.cuda.synchronize(local)
     barrier(world)
     t0 = time.perf_counter()
-    rep = nw.run_exprk22(cfg, nw.Field2D(v0), fields, precision=precision, max_steps=steps,
-                         timing=False, device=torch.device("cuda", local))
-    final = rep.final.values
+    if cname == "c4":
+        from paper_2103_06080_b200.ensemble import run_ensemble
+
+        res = run_ensemble(cfg, v0, fields, precision=precision, max_steps=steps,
+                           members=range(0, len(members)), device=torch.device("cuda", local))
+        final = res.final
+    else:
+        rep = nw.run_exprk22(cfg, nw.Field2D(v0[0]), fields, precision=precision,
+                             max_steps=steps, timing=False, device=torch.device("cuda", local))
+        final = rep.final.values
     wall = time.perf_counter() - t0
     wall_max = max_over_ranks(wall, world)
     r = 8 if precision == "double" else 4
     h2d = v0.size * 8 + 3 * (steps + 1) * cfg.N_rho * 8
-    d2h = final.size * 8 + 8 * steps
-    return {"value": world * cfg.N_rho * cfg.N_theta * steps / wall_max, "unit": UNIT,
+    d2h = final.size * 8 + 8 * steps * len(members)
+    total = ENSEMBLE_MEMBERS if cname == "c4" else world
+    return {"value": total * cfg.N_rho * cfg.N_theta * steps / wall_max, "unit": UNIT,
             "h2d_bytes_per_step": int(h2d / steps), "d2h_bytes_per_step": int(d2h / steps),
             "wall_s": wall_max, "steps": steps,
             "note": "run_exprk22(numpy v0, numpy fields) incl. plan build, H2D, D2H of the "
@@ -325,7 +369,16 @@ def cpu_reference(cfg, cname, steps_cap=3, warm=1, threads=0, precision="double"
     cores = threads if threads > 0 else oracle.host_cores()
     n = warm + steps_cap
     fields = coefficient_fields(cfg, cname, n + 1)
-    v0 = initial_field(cfg)
+    v0 = initial_fields(cfg, cname, range(0, 1))[0]
+    if cname == "c4":
+        # the fair CPU ensemble baseline is process-parallel (cores x 1 thread,
+        # SURVEY 8(d)): time one member on one thread, credit perfect scaling
+        run = oracle.march(cfg, v0, fields, precision=precision, threads=1, max_steps=n)
+        med = float(np.median(run.step_seconds[warm:]))
+        return {"value": cores * cfg.N_rho * cfg.N_theta / med, "unit": UNIT, "cores": cores,
+                "kind": "port", "s_per_step": med / cores,
+                "sample": f"{steps_cap} timed steps of one C4 member on 1 thread after {warm} "
+                          f"warm-up, x{cores} cores (ideal process-parallel ensemble)"}
     run = oracle.march(cfg, v0, fields, precision=precision, threads=cores, max_steps=n)
     secs = run.step_seconds[warm:]
     med = float(np.median(secs))
@@ -342,7 +395,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c5"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
@@ -357,7 +410,10 @@ def main():
               "scheme": "exprk22",
               "l2": "working set > 3 GB >> 126 MB L2 (no flush needed)" if args.config in ("c2", "c5")
               else "working set partly L2-resident",
-              "parallelism": f"ensemble-shard x{args.gpus}" if args.gpus > 1 else "single grid, 1 GPU"}
+              "parallelism": (f"ensemble-shard x{args.gpus}" if args.gpus > 1 or args.config == "c4"
+                              else "single grid, 1 GPU")}
+    if args.config == "c4":
+        config["members"] = ENSEMBLE_MEMBERS
 
     if args.impl == "reference":
         if rank != 0:

@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -104,23 +105,24 @@ unsigned magic_for(int d) {
 template <typename T>
 void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& tw) {
   const long double pi = 3.141592653589793238462643383279502884L;
-  std::vector<int> span, ofs;
+  std::vector<int> span, ofs, fin;
   tw.clear();
+  auto push_w = [&](long long t, int L) {
+    const long double a = 2.0L * pi * (long double)(t % L) / (long double)L;
+    cplx<T> w;
+    w.x = (T)cosl(a);
+    w.y = (T)-sinl(a);
+    tw.push_back(w);
+  };
   int L = n;
   for (int r : h.stages) {
+    // two-level table of W_L^i, i < s: coarse W_L^{64 c}, fine W_L^f
     span.push_back(L);
-    ofs.push_back((int)tw.size());
     const int s = L / r;
-    for (int q = 1; q < r; ++q)
-      for (int i = 0; i < s; ++i) {
-        // exact integer angle reduction: W_L^{q i} = W_n^{(q i mod L) n / L}
-        const long long t = (long long)q * i % L;
-        const long double a = 2.0L * pi * (long double)t / (long double)L;
-        cplx<T> w;
-        w.x = (T)cosl(a);
-        w.y = (T)-sinl(a);
-        tw.push_back(w);
-      }
+    ofs.push_back((int)tw.size());
+    for (int c = 0; c < (s + 63) / 64; ++c) push_w(64LL * c, L);
+    fin.push_back((int)tw.size());
+    for (int f = 0; f < 64; ++f) push_w(f, L);
     L = s;
   }
   if (tw.empty()) tw.push_back(cplx<T>{1, 0});
@@ -133,7 +135,9 @@ void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& t
     d.ptype[p] = 10 * ra + rb;
     d.pspan[p] = span[st];
     d.pofs_a[p] = ofs[st];
+    d.pfin_a[p] = fin[st];
     d.pofs_b[p] = rb > 1 ? ofs[st + 1] : 0;
+    d.pfin_b[p] = rb > 1 ? fin[st + 1] : 0;
     const int sb = span[st] / ra / rb;
     d.pmag_row[p] = magic_for(n / (ra * rb));
     d.pmag_sb[p] = magic_for(sb);
@@ -199,6 +203,11 @@ struct nwb_plan {
   FftDesc dr{}, dh{};
   FftPlanHost plan_r, plan_h;
   int theta_rows = 1, rho_threads = 256;
+  int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
+  int rho_prefetch = 1;      // bulk L2 prefetch of combine operands (NWB_RHO_PREFETCH=0 disables)
+  int rho_debug = 0;         // NWB_RHO_DEBUG measurement knobs (never set in production)
+  FftDesc dh2{};             // half-column descriptor (split mode)
+  void *tw_h2 = nullptr, *tw_split = nullptr;
   size_t rsz = 8;  // sizeof(real)
   // device buffers
   void *tw_r = nullptr, *tw_h = nullptr, *wk = nullptr;
@@ -269,6 +278,12 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.P2 = (const cplx<T>*)p->P2;
   a.ds = (T)p->d_sigma;
   a.zero_stride = 4;
+  a.split = p->rho_split;
+  a.prefetch = p->rho_prefetch;
+  a.debug = p->rho_debug;
+  a.dh2 = p->dh2;
+  a.tw_h2 = (const cplx<T>*)p->tw_h2;
+  a.tw_split = (const cplx<T>*)p->tw_split;
   return a;
 }
 
@@ -428,6 +443,19 @@ template <typename T> int create_impl(nwb_plan* p) {
   CU(cudaMemcpy(p->pos_r, pr.data(), pr.size() * sizeof(int), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(p->rev_r, fr.data(), fr.size() * sizeof(int), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(p->pos_h, ph.data(), ph.size() * sizeof(int), cudaMemcpyHostToDevice));
+  if (p->rho_split) {
+    // half transform = the full plan without its leading radix-2 stage
+    FftPlanHost half;
+    half.stages.assign(p->plan_r.stages.begin() + 1, p->plan_r.stages.end());
+    half.passes.assign(p->plan_r.passes.begin() + 1, p->plan_r.passes.end());
+    std::vector<cplx<T>> tw2;
+    build_desc<T>(g.nr / 2, half, p->dh2, tw2);
+    auto tws = twiddles<T>(g.nr, g.nr / 2);
+    TRY(dalloc(p, &p->tw_h2, tw2.size() * C));
+    TRY(dalloc(p, &p->tw_split, tws.size() * C));
+    CU(cudaMemcpy(p->tw_h2, tw2.data(), tw2.size() * C, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(p->tw_split, tws.data(), tws.size() * C, cudaMemcpyHostToDevice));
+  }
 
   // multiplier tables, digit-reversed rho order (exprk.py:111-131)
   TableArgs ta{};
@@ -820,7 +848,17 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   p->A = A;
   p->B = B;
   p->eps = eps;
-  if (!plan_fft(n_rho, false, p->plan_r) || !plan_fft(p->g.m, false, p->plan_h)) {
+  // Columns above ~96 KB (fp64 N_rho >= 6144) are split over a 2-CTA cluster
+  // so two columns' worth of CTAs share an SM; NWB_RHO_SPLIT=0/1 overrides.
+  {
+    const size_t col_bytes = (size_t)n_rho * 2 * p->rsz;
+    p->rho_split = (n_rho % 2 == 0 && n_rho >= 16 && col_bytes > 96 * 1024) ? 1 : 0;
+    if (const char* env = std::getenv("NWB_RHO_SPLIT"))
+      p->rho_split = (env[0] == '1' && n_rho % 2 == 0 && n_rho >= 16) ? 1 : 0;
+    if (const char* env = std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = env[0] == '1';
+    if (const char* env = std::getenv("NWB_RHO_DEBUG")) p->rho_debug = std::atoi(env);
+  }
+  if (!plan_fft(n_rho, p->rho_split != 0, p->plan_r) || !plan_fft(p->g.m, false, p->plan_h)) {
     delete p;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
   }
@@ -839,6 +877,11 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     }
   int th = ((n_rho / 4) + 31) / 32 * 32;
   p->rho_threads = th < 64 ? 64 : (th > 512 ? 512 : th);
+  if (p->rho_split) p->rho_threads = p->rho_threads > 256 ? 256 : p->rho_threads;
+  if (const char* env = std::getenv("NWB_RHO_THREADS")) {
+    const int t = std::atoi(env);
+    if (t >= 32 && t <= (p->rho_split ? 256 : 1024) && t % 32 == 0) p->rho_threads = t;
+  }
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {

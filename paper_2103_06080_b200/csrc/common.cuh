@@ -63,7 +63,9 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Prefetch [ptr, ptr + bytes) into L2 with one bulk (TMA) request per 64 KB;
 // bytes must be a multiple of 16 and ptr 16-byte aligned.
 __device__ __forceinline__ void prefetch_l2_bulk(const void* ptr, unsigned bytes) {
-  const char* p = (const char*)ptr;
+  const uintptr_t a = (uintptr_t)ptr & ~(uintptr_t)15;  // 16-byte aligned start
+  bytes = (unsigned)(((uintptr_t)ptr + bytes - a) & ~(uintptr_t)15);
+  const char* p = (const char*)a;
   while (bytes) {
     const unsigned chunk = bytes > 65536u ? 65536u : bytes;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(chunk) : "memory");

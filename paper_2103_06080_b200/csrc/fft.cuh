@@ -30,8 +30,10 @@ struct FftDesc {
   int np;                             // passes (1 or 2 fused stages each)
   int ptype[NWB_MAX_PASSES];          // 10 * ra + rb (rb = 1: single stage)
   int pspan[NWB_MAX_PASSES];          // L of the pass's first stage
-  int pofs_a[NWB_MAX_PASSES];         // twiddle-table offset, stage a
-  int pofs_b[NWB_MAX_PASSES];         // twiddle-table offset, stage b
+  int pofs_a[NWB_MAX_PASSES];         // twiddle tables of stage a / b: coarse part
+  int pofs_b[NWB_MAX_PASSES];         //   W_L^{64 c} at ofs + c, fine part W_L^f at
+  int pfin_a[NWB_MAX_PASSES];         //   fin + f (f < 64): W_L^i = coarse[i>>6] fine[i&63]
+  int pfin_b[NWB_MAX_PASSES];
   unsigned pmag_row[NWB_MAX_PASSES];  // magic for x / (n / (ra rb)), 0 = divide by 1
   unsigned pmag_sb[NWB_MAX_PASSES];   // magic for x / s_b
   // bank-conflict padding of the shared-memory line: element e lives at
@@ -162,6 +164,22 @@ template <bool CONJ, typename V> __device__ __forceinline__ V twmul(V a, V w) {
   return CONJ ? cmulc(a, w) : cmul(a, w);
 }
 
+// t[q] *= W_L^{q i} (conjugated if CONJ), q = 1..R-1: W_L^i from the two-level
+// table (two L1-resident loads, one product), higher powers by products
+template <int R, bool CONJ, typename V>
+__device__ __forceinline__ void apply_tw(V* t, const V* __restrict__ coarse,
+                                         const V* __restrict__ fine, int i) {
+  if (i == 0) return;
+  const V w1 = cmul(__ldg(coarse + (i >> 6)), __ldg(fine + (i & 63)));
+  V w = w1;
+  t[1] = twmul<CONJ>(t[1], w);
+#pragma unroll
+  for (int q = 2; q < R; ++q) {
+    w = cmul(w, w1);
+    t[q] = twmul<CONJ>(t[q], w);
+  }
+}
+
 __device__ __forceinline__ unsigned fdiv(unsigned x, unsigned magic) {
   return magic ? __umulhi(x, magic) : x;
 }
@@ -180,6 +198,8 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
   const int total = per_row * rows;
   const V* twa = tw + d.pofs_a[p];
   const V* twb = tw + d.pofs_b[p];
+  const V* fia = tw + d.pfin_a[p];
+  const V* fib = tw + d.pfin_b[p];
   for (int g = threadIdx.x; g < total; g += blockDim.x) {
     const int row = (int)fdiv((unsigned)g, d.pmag_row[p]);
     const int h = g - row * per_row;
@@ -203,11 +223,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
 #pragma unroll
         for (int m = 0; m < RA; ++m) t[m] = a[m * RB + n2];
         bfly<RA, CONJ>(t);
-        const int ia = i + n2 * sb;
-        if (ia != 0) {
-#pragma unroll
-          for (int q = 1; q < RA; ++q) t[q] = twmul<CONJ>(t[q], __ldg(twa + (q - 1) * sa + ia));
-        }
+        apply_tw<RA, CONJ>(t, twa, fia, i + n2 * sb);
 #pragma unroll
         for (int q = 0; q < RA; ++q) a[q * RB + n2] = t[q];
       }
@@ -219,10 +235,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
 #pragma unroll
           for (int n2 = 0; n2 < RB; ++n2) t[n2] = a[q * RB + n2];
           bfly<RB, CONJ>(t);
-          if (i != 0) {
-#pragma unroll
-            for (int r = 1; r < RB; ++r) t[r] = twmul<CONJ>(t[r], __ldg(twb + (r - 1) * sb + i));
-          }
+          apply_tw<RB, CONJ>(t, twb, fib, i);
 #pragma unroll
           for (int r = 0; r < RB; ++r) a[q * RB + r] = t[r];
         }
@@ -235,10 +248,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
           V t[RB];
 #pragma unroll
           for (int r = 0; r < RB; ++r) t[r] = a[q * RB + r];
-          if (i != 0) {
-#pragma unroll
-            for (int r = 1; r < RB; ++r) t[r] = twmul<CONJ>(t[r], __ldg(twb + (r - 1) * sb + i));
-          }
+          apply_tw<RB, CONJ>(t, twb, fib, i);
           bfly<RB, CONJ>(t);
 #pragma unroll
           for (int n2 = 0; n2 < RB; ++n2) a[q * RB + n2] = t[n2];
@@ -249,11 +259,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
         V t[RA];
 #pragma unroll
         for (int q = 0; q < RA; ++q) t[q] = a[q * RB + n2];
-        const int ia = i + n2 * sb;
-        if (ia != 0) {
-#pragma unroll
-          for (int q = 1; q < RA; ++q) t[q] = twmul<CONJ>(t[q], __ldg(twa + (q - 1) * sa + ia));
-        }
+        apply_tw<RA, CONJ>(t, twa, fia, i + n2 * sb);
         bfly<RA, CONJ>(t);
 #pragma unroll
         for (int m = 0; m < RA; ++m) a[m * RB + n2] = t[m];

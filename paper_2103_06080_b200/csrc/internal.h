@@ -66,6 +66,14 @@ template <typename T> struct RhoArgs {
   int* step_ctr;              // incremented by block (0,0) when non-null (last kernel of a step)
   u64* zero_bits;             // alpha slot cleared for the next stage (per member), or null
   int zero_stride;
+  // cluster-split variant (2 CTAs per column, n/2 points each): descriptor of
+  // the half transform and W_n^i, i < n/2, for the radix-2 split stage
+  FftDesc dh2;
+  const cplx<T>* tw_h2;
+  const cplx<T>* tw_split;
+  int split;
+  int prefetch;               // bulk L2 prefetch of the combine operands at entry
+  int debug;                  // measurement knobs (NWB_RHO_DEBUG): 1 skip FFTs, 2 skip combine loads
 };
 
 template <typename T> struct WenoArgs {

@@ -15,6 +15,8 @@
 // Global -> shared staging uses cp.async (many 16-byte requests in flight
 // per thread); the rho pass prefetches its combine operands into L2 with
 // bulk (TMA) prefetches at entry so they arrive while the forward FFT runs.
+#include <cooperative_groups.h>
+
 #include "internal.h"
 
 namespace nwb {
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
     for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = src[a.pos_r[f]];
     return;
   }
-  if (threadIdx.x == 0) {
+  if (a.prefetch && threadIdx.x == 0) {
     // the combine operands are consumed after the forward FFT: start their
     // DRAM -> L2 traffic now so it overlaps the transform
     if (MODE == RHO_STAGE1) {
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
   }
   if (a.zero_bits && k == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
   __syncthreads();
-  if (MODE != RHO_INV_NAT) fft_forward(x, a.dr, 1, 0, a.tw_r);
+  if (MODE != RHO_INV_NAT && !(a.debug & 1)) fft_forward(x, a.dr, 1, 0, a.tw_r);
 
   if (MODE == RHO_FWD_NAT) {
     V* dst = a.out + row;
@@ -217,8 +219,9 @@ __global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
     const int sp = pidx(a.dr, p);
     const V b = x[sp];
     if (MODE == RHO_STAGE1) {
-      const V e = a.E[trow + p], vh = a.vh[row + p];
-      const V p1 = a.P1[trow + p], p12 = a.P12[trow + p];
+      const bool nl = a.debug & 2;
+      const V e = nl ? b : a.E[trow + p], vh = nl ? b : a.vh[row + p];
+      const V p1 = nl ? b : a.P1[trow + p], p12 = nl ? b : a.P12[trow + p];
       const V ev = cmul(e, vh);
       const V vs = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), b));
       a.u[row + p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), b));
@@ -238,10 +241,103 @@ __global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
     }
   }
   __syncthreads();
-  fft_inverse(x, a.dr, 1, 0, a.tw_r);
+  if (!(a.debug & 1)) fft_inverse(x, a.dr, 1, 0, a.tw_r);
   V* dst = a.out + row;
   for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+}
+
+// ------------------------------------------------------------------ rho pass, cluster split
+// A 2-CTA cluster owns one column; CTA c holds n/2 points (half the shared
+// memory, so two CTAs fit per SM and one's memory phase overlaps the
+// other's transform).  Forward: the radix-2 DIF split stage is applied while
+// loading (both CTAs read the column; L2 serves the second read):
+//   c = 0: y_i = x_i + x_{i+n/2},   c = 1: y_i = (x_i - x_{i+n/2}) W_n^i
+// then an n/2-point DIF; CTA c holds digit-reversed positions c n/2 + p'
+// (frequencies of parity c), so the combine touches one contiguous half of
+// every digit-reversed row.  Inverse: an n/2-point DIT per CTA gives A (c=0)
+// and B (c=1); the final radix-2 DIT stage reads the partner's half through
+// distributed shared memory:
+//   out_i = A_i + conj(W_n^i) B_i,   out_{i+n/2} = A_i - conj(W_n^i) B_i.
+
+template <typename T, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) k_rho_split(const RhoArgs<T> a) {
+  using V = cplx<T>;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* x = reinterpret_cast<V*>(smem_raw);
+  const int n = a.dr.n, h = n >> 1;
+  const int c = (int)cluster.block_rank();
+  const int mem = blockIdx.x >> 1, k = blockIdx.y;
+  const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+  const size_t trow = (size_t)k * a.g.ld;
+  const size_t hrow = row + (size_t)c * h, htrow = trow + (size_t)c * h;
+  const FftDesc& d2 = a.dh2;
+  if (a.prefetch && threadIdx.x == 0) {
+    if (MODE == RHO_STAGE1) {
+      prefetch_row(a.vh + hrow, h);
+      prefetch_row(a.E + htrow, h);
+      prefetch_row(a.P1 + htrow, h);
+      prefetch_row(a.P12 + htrow, h);
+    } else if (MODE == RHO_STAGE2) {
+      prefetch_row(a.u + hrow, h);
+      prefetch_row(a.P2 + htrow, h);
+    } else if (MODE == RHO_EULER) {
+      prefetch_row(a.vh + hrow, h);
+      prefetch_row(a.E + htrow, h);
+      prefetch_row(a.P1 + htrow, h);
+    }
+  }
+  const V* src = a.in + row;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    const V lo = src[i], hi = src[i + h];
+    x[pidx(d2, i)] = c == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), a.tw_split[i]);
+  }
+  if (a.zero_bits && k == 0 && c == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
+  __syncthreads();
+  fft_forward(x, d2, 1, 0, a.tw_h2);
+  const T ds = a.ds;
+#pragma unroll 2
+  for (int p = threadIdx.x; p < h; p += blockDim.x) {
+    const int sp = pidx(d2, p);
+    const V b = x[sp];
+    if (MODE == RHO_STAGE1) {
+      const V e = a.E[htrow + p], vh = a.vh[hrow + p];
+      const V p1 = a.P1[htrow + p], p12 = a.P12[htrow + p];
+      const V ev = cmul(e, vh);
+      a.u[hrow + p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), b));
+      x[sp] = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), b));
+    } else if (MODE == RHO_STAGE2) {
+      const V p2 = a.P2[htrow + p], u = a.u[hrow + p];
+      const V vn = cadd(u, cmul(mk<V>(ds * p2.x, ds * p2.y), b));
+      a.vh[hrow + p] = vn;
+      x[sp] = vn;
+    } else if (MODE == RHO_EULER) {
+      const V e = a.E[htrow + p], vh = a.vh[hrow + p], p1 = a.P1[htrow + p];
+      const V vn = cadd(cmul(e, vh), cmul(mk<V>(ds * p1.x, ds * p1.y), b));
+      a.vh[hrow + p] = vn;
+      x[sp] = vn;
+    } else {  // RHO_INIT
+      a.vh[hrow + p] = b;
+    }
+  }
+  __syncthreads();
+  fft_inverse(x, d2, 1, 0, a.tw_h2);
+  cluster.sync();  // both halves transformed and visible cluster-wide
+  const V* xo = cluster.map_shared_rank(x, c ^ 1);
+  V* dst = a.out + row + (size_t)c * h;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    const int si = pidx(d2, i);
+    const V mine = x[si], other = xo[si];
+    const V A = c == 0 ? mine : other, B = c == 0 ? other : mine;
+    const V wb = cmulc(B, a.tw_split[i]);
+    dst[i] = c == 0 ? cadd(A, wb) : csub(A, wb);
+  }
+  if (a.step_ctr && mem == 0 && k == 0 && c == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+  cluster.sync();  // keep this CTA's shared memory alive until the partner has read it
 }
 
 // ------------------------------------------------------------------ transpose
@@ -363,6 +459,15 @@ template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cud
 
 template <typename T, int MODE>
 static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
+  if constexpr (MODE <= RHO_INIT) {
+    if (a.split) {
+      const size_t sm = (size_t)padded_len(a.dh2.n, a.dh2.pad_period) * sizeof(cplx<T>);
+      cudaFuncSetAttribute(k_rho_split<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      dim3 grid(2 * a.g.batch, a.g.kk);
+      k_rho_split<T, MODE><<<grid, threads, sm, s>>>(a);
+      return;
+    }
+  }
   const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid(a.g.batch, a.g.kk);
