@@ -140,7 +140,9 @@ int nwb_tables(int precision, int n_rho, int n_theta, double rho_span, double th
 int nwb_phi(const void* z_dev, long long n, int shift, void* out_dev, void* stream);
 /* Elementwise combines with numpy rounding (no FMA):
  * mode 0: out = E*vh; 1: out = vh + (ds*P1)*b1; 2: out = vh + ds*(P12*b1 + P2*b2);
- * 3: out = E*vh + (ds*P1)*b1. */
+ * 3: out = E*vh + (ds*P1)*b1.  Adding 8 rounds complex products the way
+ * numpy's AVX2/AVX-512 loops do (re = fma(ar, br, -(ai bi)),
+ * im = fma(ar, bi, ai br)) instead of numpy's scalar loop. */
 int nwb_combine(int precision, long long n, int mode, double d_sigma, const void* E_dev,
                 const void* P1_dev, const void* P12_dev, const void* P2_dev,
                 const void* vh_dev, const void* b1_dev, const void* b2_dev, void* out_dev,

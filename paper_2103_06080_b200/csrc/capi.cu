@@ -1022,7 +1022,7 @@ int nwb_phi(const void* z, long long n, int shift, void* out, void* stream) {
 int nwb_combine(int precision, long long n, int mode, double ds, const void* E, const void* P1,
                 const void* P12, const void* P2, const void* vh, const void* b1, const void* b2,
                 void* out, void* stream) {
-  if (mode < 0 || mode > 3) return fail(NWB_EINVAL, "unknown combine mode");
+  if ((mode & 7) > 3 || mode < 0 || mode > 15) return fail(NWB_EINVAL, "unknown combine mode");
   if (n <= 0) return NWB_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (precision == NWB_F64)

@@ -380,7 +380,14 @@ __device__ __forceinline__ float rn_mul(float a, float b) { return __fmul_rn(a, 
 __device__ __forceinline__ float rn_add(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ float rn_sub(float a, float b) { return __fsub_rn(a, b); }
 
-template <typename V> __device__ __forceinline__ V np_mul(V a, V b) {
+__device__ __forceinline__ double rn_fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float rn_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+// numpy's complex product: scalar loops round every product; the AVX2/AVX-512
+// loops fuse one product into each sum: re = fma(ar, br, -(ai bi)),
+// im = fma(ar, bi, ai br).  The host layer detects which one its numpy uses.
+template <bool FMA, typename V> __device__ __forceinline__ V np_mul(V a, V b) {
+  if (FMA) return mk<V>(rn_fma(a.x, b.x, -rn_mul(a.y, b.y)), rn_fma(a.x, b.y, rn_mul(a.y, b.x)));
   return mk<V>(rn_sub(rn_mul(a.x, b.x), rn_mul(a.y, b.y)), rn_add(rn_mul(a.x, b.y), rn_mul(a.y, b.x)));
 }
 template <typename V> __device__ __forceinline__ V np_add(V a, V b) {
@@ -392,7 +399,7 @@ template <typename V> __device__ __forceinline__ V np_scale(decltype(V::x) s, V 
                rn_add(rn_mul(s, a.y), rn_mul((decltype(V::x))0, a.x)));
 }
 
-template <typename T>
+template <typename T, bool FMA>
 __global__ void k_combine(long n, int mode, T ds, const cplx<T>* E, const cplx<T>* P1,
                           const cplx<T>* P12, const cplx<T>* P2, const cplx<T>* vh,
                           const cplx<T>* b1, const cplx<T>* b2, cplx<T>* out) {
@@ -400,13 +407,13 @@ __global__ void k_combine(long n, int mode, T ds, const cplx<T>* E, const cplx<T
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
     V r;
     if (mode == 0) {          // ev = E * vhat
-      r = np_mul(E[i], vh[i]);
+      r = np_mul<FMA>(E[i], vh[i]);
     } else if (mode == 1) {   // vh here is ev: ev + (ds * Phi1) * bh1
-      r = np_add(vh[i], np_mul(np_scale(ds, P1[i]), b1[i]));
+      r = np_add(vh[i], np_mul<FMA>(np_scale(ds, P1[i]), b1[i]));
     } else if (mode == 2) {   // ev + ds * (Phi1m2 * bh1 + Phi2 * bh2)
-      r = np_add(vh[i], np_scale(ds, np_add(np_mul(P12[i], b1[i]), np_mul(P2[i], b2[i]))));
+      r = np_add(vh[i], np_scale(ds, np_add(np_mul<FMA>(P12[i], b1[i]), np_mul<FMA>(P2[i], b2[i]))));
     } else {                  // Euler: E * vhat + (ds * Phi1) * bh1
-      r = np_add(np_mul(E[i], vh[i]), np_mul(np_scale(ds, P1[i]), b1[i]));
+      r = np_add(np_mul<FMA>(E[i], vh[i]), np_mul<FMA>(np_scale(ds, P1[i]), b1[i]));
     }
     out[i] = r;
   }
@@ -497,7 +504,11 @@ template <typename T>
 void launch_combine(long n, int mode, double ds, const cplx<T>* E, const cplx<T>* P1,
                     const cplx<T>* P12, const cplx<T>* P2, const cplx<T>* vh,
                     const cplx<T>* b1, const cplx<T>* b2, cplx<T>* out, cudaStream_t s) {
-  k_combine<T><<<grid_cap(n, 256), 256, 0, s>>>(n, mode, (T)ds, E, P1, P12, P2, vh, b1, b2, out);
+  // mode bit 3 selects numpy's SIMD (fused) complex-product rounding
+  if (mode & 8)
+    k_combine<T, true><<<grid_cap(n, 256), 256, 0, s>>>(n, mode & 7, (T)ds, E, P1, P12, P2, vh, b1, b2, out);
+  else
+    k_combine<T, false><<<grid_cap(n, 256), 256, 0, s>>>(n, mode, (T)ds, E, P1, P12, P2, vh, b1, b2, out);
 }
 
 template <typename T> void launch_convert(long n, const double* in, T* out, cudaStream_t s) {

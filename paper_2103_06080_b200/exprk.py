@@ -181,12 +181,43 @@ class SpectralTransforms:
 
 # ---------------------------------------------------------------------- step API
 
+_NUMPY_FMA: dict = {}
+
+
+def numpy_cmul_is_fused(dtype=np.complex128) -> bool:
+    """Does this host's numpy round complex products with a fused multiply-add?
+
+    numpy's SIMD loops (AVX2 / AVX-512) compute re = fma(ar, br, -(ai bi)),
+    im = fma(ar, bi, ai br); its scalar loop rounds every product.  The
+    generic step API reproduces whichever this host's numpy does, so results
+    handed back to numpy callers match ``E * vhat`` bitwise (reference test
+    ``tests/test_exprk.py:131-138``).  Decided once per dtype from exact
+    rational arithmetic on a fixed sample.
+    """
+    key = np.dtype(dtype).name
+    if key not in _NUMPY_FMA:
+        from fractions import Fraction
+
+        rng = np.random.default_rng(12345)
+        a = (rng.standard_normal(64) + 1j * rng.standard_normal(64)).astype(dtype)
+        b = (rng.standard_normal(64) + 1j * rng.standard_normal(64)).astype(dtype)
+        c = a * b
+        real_t = a.real.dtype.type
+        fused = [real_t(float(Fraction(float(x.real)) * Fraction(float(y.real))
+                              + Fraction(float(-(x.imag * y.imag)))))
+                 for x, y in zip(a, b)]
+        _NUMPY_FMA[key] = bool(np.array_equal(c.real, np.array(fused, dtype=real_t)))
+    return _NUMPY_FMA[key]
+
+
 def _combine(mode, d_sigma, tables, vh, b1=None, b2=None):
     torch = _torch()
     lib = _lib.lib()
     E, P1, P12, P2 = tables
     out = torch.empty_like(vh)
     prec = _lib.F64 if vh.dtype == torch.complex128 else _lib.F32
+    if numpy_cmul_is_fused(np.complex128 if prec == _lib.F64 else np.complex64):
+        mode |= 8
     check(lib.nwb_combine(prec, vh.numel(), mode, float(d_sigma), ptr(E), ptr(P1), ptr(P12),
                           ptr(P2), ptr(vh), ptr(b1), ptr(b2), ptr(out),
                           torch.cuda.current_stream(vh.device).cuda_stream), "nwb_combine")
