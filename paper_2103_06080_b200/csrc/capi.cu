@@ -231,17 +231,39 @@ struct nwb_plan {
 
 namespace {
 
+// Workspaces come from the device's stream-ordered memory pool with an
+// unbounded release threshold: destroying a plan returns its gigabytes to the
+// pool without a device-wide synchronising cudaFree, and the next plan of the
+// same size is served from the pool (plan churn in studies costs ~nothing).
+void keep_pool_memory(int device) {
+  static bool done[64] = {false};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 int dalloc(nwb_plan* p, void** ptr, size_t bytes) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(ptr, bytes);
+  cudaError_t e = cudaMallocAsync(ptr, bytes, p->stream);
   if (e != cudaSuccess) {
     *ptr = nullptr;
     return fail(e == cudaErrorMemoryAllocation ? NWB_ENOMEM : NWB_ECUDA,
-                std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+                std::string("cudaMallocAsync(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
   }
   p->allocs.push_back(*ptr);
   p->bytes += (long long)bytes;
   return NWB_OK;
+}
+
+void dfree(nwb_plan* p, void* ptr) {
+  if (!ptr) return;
+  cudaFreeAsync(ptr, p->stream);
+  for (auto& x : p->allocs)
+    if (x == ptr) x = nullptr;
 }
 
 #define TRY(x)                 \
@@ -367,11 +389,7 @@ template <typename T> void launch_step(nwb_plan* p, int scheme, cudaEvent_t* ev)
 // per-step guard history [batch][len]; reallocation invalidates captured graphs
 int ensure_hist(nwb_plan* p, int len) {
   if (p->hist_len >= len && p->vmax_hist) return NWB_OK;
-  if (p->vmax_hist) {
-    cudaFree(p->vmax_hist);
-    for (auto& x : p->allocs)
-      if (x == p->vmax_hist) x = nullptr;
-  }
+  dfree(p, p->vmax_hist);
   p->vmax_hist = nullptr;
   p->hist_len = len;
   TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)p->g.batch * len * sizeof(u64)));
@@ -478,13 +496,7 @@ template <typename T> int set_coeffs_impl(nwb_plan* p, const double* up, const d
                                           const double* du, int n_rows, int ld, int on_dev) {
   const Geom& g = p->g;
   const size_t n = (size_t)n_rows * g.nr;
-  for (void* a : {p->upar, p->uperp, p->du, (void*)p->alpha_rho}) {
-    if (a) {
-      cudaFree(a);
-      for (auto& x : p->allocs)
-        if (x == a) x = nullptr;
-    }
-  }
+  for (void* a : {p->upar, p->uperp, p->du, (void*)p->alpha_rho}) dfree(p, a);
   p->upar = p->uperp = p->du = nullptr;
   p->alpha_rho = nullptr;
   TRY(dalloc(p, &p->upar, n * sizeof(T)));
@@ -499,7 +511,7 @@ template <typename T> int set_coeffs_impl(nwb_plan* p, const double* up, const d
     }
   TRY(ensure_hist(p, n_rows));
   double* stage = nullptr;
-  CU(cudaMalloc(&stage, n * sizeof(double)));
+  CU(cudaMallocAsync(&stage, n * sizeof(double), p->stream));
   const double* srcs[3] = {up, uq, du};
   void* dsts[3] = {p->upar, p->uperp, p->du};
   for (int i = 0; i < 3; ++i) {
@@ -513,8 +525,8 @@ template <typename T> int set_coeffs_impl(nwb_plan* p, const double* up, const d
     launch_convert<T>((long)n, stage, (T*)dsts[i], p->stream);
   }
   launch_alpha_rho<T>((const T*)p->uperp, g.nr, n_rows, p->alpha_rho, p->stream);
+  cudaFreeAsync(stage, p->stream);
   cudaError_t e = cudaStreamSynchronize(p->stream);
-  cudaFree(stage);
   if (e != cudaSuccess) return fail(NWB_ECUDA, std::string("set_coeffs: ") + cudaGetErrorString(e));
   CHECK_LAUNCH("set_coeffs");
   return NWB_OK;
@@ -848,11 +860,11 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   p->A = A;
   p->B = B;
   p->eps = eps;
-  // Columns above ~96 KB (fp64 N_rho >= 6144) are split over a 2-CTA cluster
-  // so two columns' worth of CTAs share an SM; NWB_RHO_SPLIT=0/1 overrides.
+  // The 2-CTA cluster split of a rho column (k_rho_split) is available but off
+  // by default: measured at Set 4 fp64 it loses to one CTA per column
+  // (0.93 vs 0.79 ms, profiles/README.md); NWB_RHO_SPLIT=1 enables it.
   {
-    const size_t col_bytes = (size_t)n_rho * 2 * p->rsz;
-    p->rho_split = (n_rho % 2 == 0 && n_rho >= 16 && col_bytes > 96 * 1024) ? 1 : 0;
+    p->rho_split = 0;
     if (const char* env = std::getenv("NWB_RHO_SPLIT"))
       p->rho_split = (env[0] == '1' && n_rho % 2 == 0 && n_rho >= 16) ? 1 : 0;
     if (const char* env = std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = env[0] == '1';
@@ -889,6 +901,7 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     return fail(NWB_ECUDA, std::string("plan device/stream: ") + cudaGetErrorString(e));
   }
   p->stream = p->own_stream;
+  keep_pool_memory(device);
   int rc = precision == NWB_F64 ? create_impl<double>(p) : create_impl<float>(p);
   if (rc != NWB_OK) {
     nwb_plan_destroy(p);
@@ -905,7 +918,7 @@ int nwb_plan_destroy(nwb_plan* p) {
   for (int i = 0; i < 2; ++i)
     if (p->graph[i]) cudaGraphExecDestroy(p->graph[i]);
   for (void* a : p->allocs)
-    if (a) cudaFree(a);
+    if (a) cudaFreeAsync(a, p->stream);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
   delete p;
   return NWB_OK;

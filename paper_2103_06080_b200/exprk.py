@@ -306,6 +306,16 @@ def _snapshot_steps(config: DomainConfig, snapshot_sigmas) -> dict[int, float]:
     return plan
 
 
+def _to_host64(t) -> np.ndarray:
+    """Device tensor -> fresh float64 numpy array (cast on the device, one
+    cudaMemcpy into the destination; ~2x faster than Tensor.cpu())."""
+    torch = _torch()
+    src = t.to(torch.float64).contiguous()
+    out = np.empty(tuple(src.shape), dtype=np.float64)
+    torch.from_numpy(out).copy_(src)
+    return out
+
+
 def _as_host_field(x) -> np.ndarray:
     torch = _torch()
     if isinstance(x, torch.Tensor):
@@ -363,9 +373,8 @@ def run_exprk22(config: DomainConfig, v0, fields, snapshot_sigmas=None,
         if not np.isfinite(m) or m > guard:
             raise InstabilityError(n_steps * config.d_sigma, m)
         max_abs_v = max(float(np.max(max_abs)) if n_steps else 0.0, m)
-        final = Field2D(v_fin[0].to("cpu", torch.float64).numpy())
-        snapshots = {snap_plan[n]: Field2D(b[0].to("cpu", torch.float64).numpy())
-                     for n, b in sorted(bufs.items())}
+        final = Field2D(_to_host64(v_fin[0]))
+        snapshots = {snap_plan[n]: Field2D(_to_host64(b[0])) for n, b in sorted(bufs.items())}
         if n_steps in snap_plan:
             snapshots[snap_plan[n_steps]] = final.copy()
         wall = time.perf_counter() - t_start
