@@ -234,7 +234,9 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
     # dominant kernel type by summed time over the step
     by_kernel = {}
     for p in per:
-        d = by_kernel.setdefault(p["kernel"], {"ms": 0.0, "bytes": 0, "n": 0})
+        # both rho stages are launches of the same kernel (k_rho, two modes)
+        group = "rho_pass" if p["kernel"].startswith("rho") else p["kernel"]
+        d = by_kernel.setdefault(group, {"ms": 0.0, "bytes": 0, "n": 0})
         d["ms"] += p["ms"]; d["bytes"] += p["bytes"]; d["n"] += 1
     step_ms = sum(p["ms"] for p in per)
     dom = max(by_kernel, key=lambda k: by_kernel[k]["ms"])
