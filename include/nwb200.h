@@ -136,6 +136,16 @@ int nwb_weno5_b(int precision, int batch, int n_rho, int n_theta, const void* v_
 int nwb_tables(int precision, int n_rho, int n_theta, double rho_span, double theta_span,
                double d_sigma, double A, double eps, void* E_dev, void* P1_dev, void* P2_dev,
                void* P12_dev, void* z_dev, void* stream);
+/* Random-mode velocity fields on the device (turbulence.py:145-203, SURVEY
+ * row f1): mode_params_dev = [kx | ky | phase | amp1 | amp2 | w_ds | w_dr],
+ * n_modes each (w_ds = -amp2 kx lam, w_dr = -amp2 ky lam); sigma/rho nodes
+ * device float64; outputs (n_sigma, n_rho) device float64, scaled by inv_c0;
+ * scratch_dev holds 2 (n_sigma + n_rho) n_modes doubles. */
+int nwb_turbulence_fields(int n_modes, const double* mode_params_dev, double lam, double inv_c0,
+                          const double* sigma_nodes_dev, int n_sigma, const double* rho_nodes_dev,
+                          int n_rho, double* scratch_dev, double* u_par_dev, double* u_perp_dev,
+                          double* du_dsigma_dev, double* du_drho_dev, void* stream);
+
 /* phi_shift(z) for complex128 z (shift 1 or 2). */
 int nwb_phi(const void* z_dev, long long n, int shift, void* out_dev, void* stream);
 /* Elementwise combines with numpy rounding (no FMA):

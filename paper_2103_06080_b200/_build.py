@@ -52,15 +52,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _sources())
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
+          defines=(), out: str | None = None) -> str:
+    """Compile and link; ``defines``/``out`` build an experiment variant."""
+    lib_path = out or LIB_PATH
+    if not force and not defines and out is None and up_to_date():
         return LIB_PATH
-    os.makedirs(BUILD_DIR, exist_ok=True)
+    build_dir = BUILD_DIR + ("_" + os.path.basename(lib_path).replace(".so", "") if out else "")
+    os.makedirs(build_dir, exist_ok=True)
     objs = []
     procs = []
     for unit, extra in UNITS.items():
-        obj = os.path.join(BUILD_DIR, unit.replace(".cu", ".o"))
-        cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, unit), "-o", obj]
+        obj = os.path.join(build_dir, unit.replace(".cu", ".o"))
+        cmd = [nvcc(), *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c",
+               os.path.join(CSRC, unit), "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         if verbose:
@@ -77,13 +82,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False) -> 
             failed.append(unit)
     if failed:
         raise RuntimeError(f"nvcc failed for {failed}")
-    tmp = LIB_PATH + ".tmp"
+    tmp = lib_path + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, lib_path)
+    return lib_path
 
 
 if __name__ == "__main__":
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
-                ptxas_v="--ptxas" in sys.argv))
+                ptxas_v="--ptxas" in sys.argv, defines=defs, out=outs[0] if outs else None))

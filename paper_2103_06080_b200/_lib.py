@@ -14,7 +14,7 @@ from .errors import (BackendError, BudgetExceededError, InstabilityError,
                      UnsupportedSizeError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnwb200.so")
+LIB_PATH = os.environ.get("NWB_LIB") or os.path.join(HERE, "libnwb200.so")
 
 NWB_OK = 0
 NWB_EINVAL = -1
@@ -35,6 +35,7 @@ ABI_SYMBOLS = (
     "nwb_plan_load_physical", "nwb_plan_load_spectrum", "nwb_plan_store_spectrum",
     "nwb_plan_store_physical", "nwb_march", "nwb_step", "nwb_rfft2", "nwb_irfft2",
     "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine", "nwb_profile_kernels",
+    "nwb_turbulence_fields",
 )
 
 _lock = threading.Lock()
@@ -75,6 +76,9 @@ def _declare(lib):
                                c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p]),
         "nwb_phi": (c_int, [c_void_p, c_ll, c_int, c_void_p, c_void_p]),
+        "nwb_turbulence_fields": (c_int, [c_int, c_void_p, c_double, c_double, c_void_p, c_int,
+                                          c_void_p, c_int, c_void_p, c_void_p, c_void_p,
+                                          c_void_p, c_void_p, c_void_p]),
         "nwb_combine": (c_int, [c_int, c_ll, c_int, c_double, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     }

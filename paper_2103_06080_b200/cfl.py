@@ -47,5 +47,10 @@ def check_cfl_splitting(config: DomainConfig, v_max_bound: float = 5.0,
 
 
 def check_cfl_exprk(config: DomainConfig, fields, v_max_bound: float = 5.0) -> CflReport:
-    u_perp_max = float(np.max(np.abs(fields.u_perp))) if fields is not None else 0.0
+    if fields is None:
+        u_perp_max = 0.0
+    elif hasattr(fields.u_perp, "abs"):      # device tensor (device-generated medium)
+        u_perp_max = float(fields.u_perp.abs().max())
+    else:
+        u_perp_max = float(np.max(np.abs(fields.u_perp)))
     return check_cfl_splitting(config, v_max_bound, u_perp_max)

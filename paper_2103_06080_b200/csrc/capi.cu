@@ -50,13 +50,14 @@ struct FftPlanHost {
   std::vector<std::pair<int, int>> passes;  // (ra, rb)
 };
 
-bool plan_fft(int n, bool split_two, FftPlanHost& h) {
+bool plan_fft(int n, bool split_two, FftPlanHost& h, int max_prod = 16) {
   int m = n, c2 = 0, c3 = 0, c5 = 0, c7 = 0;
   while (m % 2 == 0) { m /= 2; ++c2; }
   while (m % 3 == 0) { m /= 3; ++c3; }
   while (m % 5 == 0) { m /= 5; ++c5; }
   while (m % 7 == 0) { m /= 7; ++c7; }
   if (m != 1) return false;
+  const bool big = max_prod >= 16;  // 16: pair 7.2, 5.3, 5.2, 3.4, 3.3, 4.4; 8: only 3.2 and 8
   std::vector<std::pair<int, int>> ps;
   if (split_two) {
     if (c2 == 0) return false;
@@ -64,28 +65,30 @@ bool plan_fft(int n, bool split_two, FftPlanHost& h) {
     --c2;
   }
   for (; c7 > 0; --c7) {
-    if (c2 > 0) { ps.push_back({7, 2}); --c2; } else ps.push_back({7, 1});
+    if (big && c2 > 0) { ps.push_back({7, 2}); --c2; } else ps.push_back({7, 1});
   }
   for (; c5 > 0; --c5) {
-    if (c3 > 0) { ps.push_back({5, 3}); --c3; }
-    else if (c2 > 0) { ps.push_back({5, 2}); --c2; }
+    if (big && c3 > 0) { ps.push_back({5, 3}); --c3; }
+    else if (big && c2 > 0) { ps.push_back({5, 2}); --c2; }
     else ps.push_back({5, 1});
   }
   while (c3 > 0) {
-    if (c2 >= 2) { ps.push_back({3, 4}); c2 -= 2; --c3; }
-    else if (c3 >= 2) { ps.push_back({3, 3}); c3 -= 2; }
-    else if (c2 == 1) { ps.push_back({3, 2}); --c2; --c3; }
+    if (big && c2 >= 2) { ps.push_back({3, 4}); c2 -= 2; --c3; }
+    else if (big && c3 >= 2) { ps.push_back({3, 3}); c3 -= 2; }
+    else if (c2 >= 1) { ps.push_back({3, 2}); --c2; --c3; }
     else { ps.push_back({3, 1}); --c3; }
   }
   // a leftover 8 / 4 / 2 goes first (after a forced split stage), so the last
   // pass -- the one whose unit-stride butterflies set the smem padding -- is
   // as large as possible
+  const int group = big ? 4 : 3;
   std::vector<std::pair<int, int>> head;
-  if (c2 % 4 == 3) head.push_back({8, 1});
-  if (c2 % 4 == 2) head.push_back({4, 1});
-  if (c2 % 4 == 1) head.push_back({2, 1});
+  const int rem = c2 % group;
+  if (rem == 3) head.push_back({8, 1});
+  if (rem == 2) head.push_back({4, 1});
+  if (rem == 1) head.push_back({2, 1});
   ps.insert(ps.begin() + (split_two ? 1 : 0), head.begin(), head.end());
-  for (; c2 >= 4; c2 -= 4) ps.push_back({4, 4});
+  for (; c2 >= group; c2 -= group) ps.push_back(big ? std::make_pair(4, 4) : std::make_pair(8, 1));
   if ((int)ps.size() > NWB_MAX_PASSES) return false;
   h.passes = ps;
   h.stages.clear();
@@ -203,9 +206,11 @@ struct nwb_plan {
   FftDesc dr{}, dh{};
   FftPlanHost plan_r, plan_h;
   int theta_rows = 1, rho_threads = 256;
+  int theta_stream_rows = 0;  // R of the streaming theta kernels (0 = not used)
   int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
   int rho_prefetch = 1;      // bulk L2 prefetch of combine operands (NWB_RHO_PREFETCH=0 disables)
   int rho_debug = 0;         // NWB_RHO_DEBUG measurement knobs (never set in production)
+  int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
   FftDesc dh2{};             // half-column descriptor (split mode)
   void *tw_h2 = nullptr, *tw_split = nullptr;
   size_t rsz = 8;  // sizeof(real)
@@ -303,6 +308,7 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.split = p->rho_split;
   a.prefetch = p->rho_prefetch;
   a.debug = p->rho_debug;
+  a.persistent = p->rho_persistent;
   a.dh2 = p->dh2;
   a.tw_h2 = (const cplx<T>*)p->tw_h2;
   a.tw_split = (const cplx<T>*)p->tw_split;
@@ -342,7 +348,7 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   c.row_off = stage - 1;
   c.alpha_bits = p->red + (stage - 1);
   c.vmax_bits = stage == 1 ? p->vmax_hist : nullptr;
-  launch_theta_c2r<T>(c, p->theta_rows, s);
+  launch_theta_c2r<T>(c, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
   if (ev) cudaEventRecord(ev[1], s);
   // WENO -> b
   WenoArgs<T> w = weno_args<T>(p);
@@ -355,7 +361,7 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   ThetaArgs<T> r = theta_args<T>(p);
   r.phys_in = (const T*)p->b;
   r.spec_out = (cplx<T>*)p->bt;
-  launch_theta_r2c<T>(r, p->theta_rows, s);
+  launch_theta_r2c<T>(r, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
   if (ev) cudaEventRecord(ev[3], s);
   // rho pass
   RhoArgs<T> q = rho_args<T>(p);
@@ -442,6 +448,18 @@ template <typename T> int create_impl(nwb_plan* p) {
   std::vector<cplx<T>> twr, twh;
   build_desc<T>(g.nr, p->plan_r, p->dr, twr);
   build_desc<T>(g.m, p->plan_h, p->dh, twh);
+  // march theta passes: persistent double-buffered kernels (NWB_THETA_STREAM=1;
+  // measured slower than one-shot CTAs at Set 4, so off by default)
+  p->theta_stream_rows = 0;
+  {
+    const char* env = std::getenv("NWB_THETA_STREAM");
+    if (env && env[0] == '1')
+      for (int r : {8, 4, 2, 1})
+        if (2 * (size_t)r * padded_len(g.m, p->dh.pad_period) * C <= 200 * 1024 && r <= g.nr) {
+          p->theta_stream_rows = r;
+          break;
+        }
+  }
   auto wk = twiddles<T>(g.nt, g.kk);
   auto fr = freq_of_pos(g.nr, p->plan_r.stages);
   std::vector<int> pr(g.nr);
@@ -869,8 +887,13 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
       p->rho_split = (env[0] == '1' && n_rho % 2 == 0 && n_rho >= 16) ? 1 : 0;
     if (const char* env = std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = env[0] == '1';
     if (const char* env = std::getenv("NWB_RHO_DEBUG")) p->rho_debug = std::atoi(env);
+    if (const char* env = std::getenv("NWB_RHO_PERSIST")) p->rho_persistent = env[0] == '1';
+    if (p->rho_debug) p->rho_persistent = 0;  // the knobs live in k_rho
   }
-  if (!plan_fft(n_rho, p->rho_split != 0, p->plan_r) || !plan_fft(p->g.m, false, p->plan_h)) {
+  int mp_r = 16, mp_h = 16;
+  if (const char* env = std::getenv("NWB_MAXPROD_R")) mp_r = std::atoi(env);
+  if (const char* env = std::getenv("NWB_MAXPROD_H")) mp_h = std::atoi(env);
+  if (!plan_fft(n_rho, p->rho_split != 0, p->plan_r, mp_r) || !plan_fft(p->g.m, false, p->plan_h, mp_h)) {
     delete p;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
   }
@@ -1021,6 +1044,23 @@ int nwb_tables(int precision, int n_rho, int n_theta, double rho_span, double th
   else
     launch_tables<float>(ta, (float2*)E, (float2*)P1, (float2*)P2, (float2*)P12, (double2*)z, s);
   CHECK_LAUNCH("tables");
+  return NWB_OK;
+}
+
+int nwb_turbulence_fields(int n_modes, const double* mode_params, double lam, double inv_c0,
+                          const double* sigma_nodes, int n_sigma, const double* rho_nodes,
+                          int n_rho, double* scratch, double* u_par, double* u_perp,
+                          double* du_dsigma, double* du_drho, void* stream) {
+  if (n_modes < 1 || n_sigma < 1 || n_rho < 1) return fail(NWB_EINVAL, "empty turbulence grid");
+  if (!mode_params || !sigma_nodes || !rho_nodes || !scratch || !u_par || !u_perp || !du_dsigma ||
+      !du_drho)
+    return fail(NWB_EINVAL, "null buffer");
+  const double* mp = mode_params;  // [7][n_modes]: kx, ky, phase, amp1, amp2, w_ds, w_dr
+  launch_turbulence(mp, mp + n_modes, mp + 2 * n_modes, mp + 3 * n_modes, mp + 4 * n_modes,
+                    mp + 5 * n_modes, mp + 6 * n_modes, n_modes, lam, inv_c0, sigma_nodes, n_sigma,
+                    rho_nodes, n_rho, scratch, u_par, u_perp, du_dsigma, du_drho,
+                    (cudaStream_t)stream);
+  CHECK_LAUNCH("turbulence");
   return NWB_OK;
 }
 

@@ -74,6 +74,7 @@ template <typename T> struct RhoArgs {
   int split;
   int prefetch;               // bulk L2 prefetch of the combine operands at entry
   int debug;                  // measurement knobs (NWB_RHO_DEBUG): 1 skip FFTs, 2 skip combine loads
+  int persistent;             // march modes run k_rho_stream (one CTA per SM walking columns)
 };
 
 template <typename T> struct WenoArgs {
@@ -123,5 +124,11 @@ template <typename T>
 void launch_tables(const TableArgs& a, cplx<T>* E, cplx<T>* P1, cplx<T>* P2, cplx<T>* P12,
                    double2* z, cudaStream_t s);
 void launch_phi(const double2* z, long n, int shift, double2* out, cudaStream_t s);
+// turbulence mode sum (tables.cu); scratch holds 2 (n_sig + n_rho) n_modes doubles
+void launch_turbulence(const double* kx, const double* ky, const double* ph, const double* a1,
+                       const double* a2, const double* wds, const double* wdr, int n_modes,
+                       double lam, double inv_c0, const double* sig, int n_sig, const double* rho,
+                       int n_rho, double* scratch, double* u_par, double* u_perp, double* du_ds,
+                       double* du_dr, cudaStream_t s);
 
 }  // namespace nwb

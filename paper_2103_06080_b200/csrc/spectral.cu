@@ -44,7 +44,13 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
   }
 }
 
-template <typename T> constexpr int theta_min_blocks() { return sizeof(T) == 8 ? 2 : 3; }
+#ifndef NWB_THETA_MINB64
+#define NWB_THETA_MINB64 2
+#endif
+#ifndef NWB_RHO_THREADS_LB
+#define NWB_RHO_THREADS_LB 512
+#endif
+template <typename T> constexpr int theta_min_blocks() { return sizeof(T) == 8 ? NWB_THETA_MINB64 : 3; }
 
 // ------------------------------------------------------------------ theta c2r
 // X[0..m] staged in natural order (Im of X[0], X[m] dropped as pocketfft's c2r
@@ -155,14 +161,214 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const 
   }
 }
 
+// ------------------------------------------------------------------ theta passes, streaming
+// Persistent, double-buffered variants used by the march: one CTA per SM walks
+// groups of R rows; the cp.async staging of group i+1 is in flight while group
+// i is transformed and stored, so global traffic never stalls on the
+// transform (the single-shot kernels above alternate load and compute phases
+// and sit at ~2 TB/s).  Reductions are accumulated per thread and flushed
+// with one block reduction per member.
+
+template <typename T, int R>
+__device__ __forceinline__ void c2r_issue(const ThetaArgs<T>& a, cplx<T>* z, int rs, int grp,
+                                          int gpm) {
+  using V = cplx<T>;
+  const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
+  const V* src = a.spec_in + (size_t)mem * a.g.kk * a.g.ld;
+  for (int idx = threadIdx.x; idx < a.g.kk * R; idx += blockDim.x) {
+    const int r = idx % R, k = idx / R, j = j0 + r;
+    V* slot = &z[r * rs + pidx(a.dh, k)];
+    if (j < a.g.nr) cp_async_c(slot, &src[(size_t)k * a.g.ld + j]);
+    else *slot = mk<V>(0, 0);
+  }
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(512, 1) k_theta_c2r_stream(const ThetaArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int m = a.g.m, nr = a.g.nr;
+  const int rs = padded_len(m, a.dh.pad_period);
+  V* buf[2] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + R * rs};
+  const int gpm = (nr + R - 1) / R, groups = gpm * a.g.batch;
+  const int step = a.step_ctr ? *a.step_ctr : 0;
+  const T two_pi = (T)6.283185307179586476925;
+  const int npairs = m / 2 + 1;
+  int grp = blockIdx.x, it = 0;
+  if (grp < groups) c2r_issue<T, R>(a, buf[0], rs, grp, gpm);
+  cp_async_commit();
+  u64 amax = 0, vmax = 0;
+  for (; grp < groups; grp += gridDim.x, ++it) {
+    V* z = buf[it & 1];
+    const int nxt = grp + gridDim.x;
+    if (nxt < groups) c2r_issue<T, R>(a, buf[(it + 1) & 1], rs, nxt, gpm);
+    cp_async_commit();
+    cp_async_wait_1();
+    __syncthreads();
+    const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
+    for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
+      const int r = idx / npairs, k = idx - r * npairs;
+      V* zr = z + r * rs;
+      const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
+      V xk = zr[sk];
+      V xm = zr[sm];
+      if (k == 0) { xk.y = 0; xm.y = 0; }
+      const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
+      const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), a.wk[k]);
+      zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
+      if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
+    }
+    __syncthreads();
+    fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
+    const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * nr : nullptr;
+    T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
+    for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
+      const int r = idx / m, n = idx - r * m, j = j0 + r;
+      if (j >= nr) continue;
+      const V zz = z[r * rs + pidx(a.dh, a.pos_h[n])];
+      const T v0 = zz.x * a.scale, v1 = zz.y * a.scale;
+      *reinterpret_cast<V*>(dst + (size_t)j * a.g.nt + 2 * n) = mk<V>(v0, v1);
+      const T c = up ? two_pi * up[j] : (T)0;
+      amax = max(amax, max(abs_bits(c + a.bcoef * v0), abs_bits(c + a.bcoef * v1)));
+      vmax = max(vmax, max(abs_bits(v0), abs_bits(v1)));
+    }
+    // flush the reductions when this CTA's next group belongs to another member
+    const bool flush = nxt >= groups || nxt / gpm != mem;
+    if (flush && (a.alpha_bits || a.vmax_bits)) {
+      block_max2<T>(amax, vmax,
+                    a.alpha_bits ? a.alpha_bits + (size_t)mem * a.alpha_stride : nullptr,
+                    a.vmax_bits ? a.vmax_bits + (size_t)mem * a.vmax_stride + step : nullptr);
+      amax = vmax = 0;
+    }
+    __syncthreads();  // buffer it&1 is refilled two iterations later
+  }
+  cp_async_wait_0();
+}
+
+template <typename T, int R>
+__device__ __forceinline__ void r2c_issue(const ThetaArgs<T>& a, cplx<T>* z, int rs, int grp,
+                                          int gpm) {
+  using V = cplx<T>;
+  const int m = a.g.m;
+  const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
+  const T* src = a.phys_in + (size_t)mem * a.g.nr * a.g.nt;
+  for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
+    const int r = idx / m, n = idx - r * m, j = j0 + r;
+    V* slot = &z[r * rs + pidx(a.dh, n)];
+    if (j < a.g.nr) cp_async_c(slot, reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n));
+    else *slot = mk<V>(0, 0);
+  }
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(512, 1) k_theta_r2c_stream(const ThetaArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
+  const int rs = padded_len(m, a.dh.pad_period);
+  V* buf[2] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + R * rs};
+  const int gpm = (nr + R - 1) / R, groups = gpm * a.g.batch;
+  const int npairs = m / 2 + 1;
+  const T half = (T)0.5;
+  int grp = blockIdx.x, it = 0;
+  if (grp < groups) r2c_issue<T, R>(a, buf[0], rs, grp, gpm);
+  cp_async_commit();
+  for (; grp < groups; grp += gridDim.x, ++it) {
+    V* z = buf[it & 1];
+    const int nxt = grp + gridDim.x;
+    if (nxt < groups) r2c_issue<T, R>(a, buf[(it + 1) & 1], rs, nxt, gpm);
+    cp_async_commit();
+    cp_async_wait_1();
+    __syncthreads();
+    fft_forward(z, a.dh, R, rs, a.tw_h);
+    const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
+    V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
+    for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
+      const int r = idx % R, k = idx / R, j = j0 + r;
+      if (j >= nr) continue;
+      const V zk = z[r * rs + pidx(a.dh, a.pos_h[k])];
+      const V zm = z[r * rs + pidx(a.dh, a.pos_h[k == 0 ? 0 : m - k])];
+      const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
+      const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
+      const V wz = cmul(a.wk[k], zo);
+      dst[(size_t)k * ld + j] = cadd(ze, wz);
+      if (2 * k != m) {
+        const V d = csub(ze, wz);
+        dst[(size_t)(m - k) * ld + j] = mk<V>(d.x, -d.y);
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait_0();
+}
+
 // ------------------------------------------------------------------ rho pass
 
 template <typename V> __device__ __forceinline__ void prefetch_row(const V* p, int n) {
   prefetch_l2_bulk(p, (unsigned)((size_t)n * sizeof(V)) & ~15u);
 }
 
+// The stage combine of exprk.py:161-173 on one (half) column in
+// digit-reversed order.  Operands of U elements per thread are loaded before
+// any result is stored (the row pointers are __restrict__), so each thread
+// keeps 4U independent 16-byte loads in flight -- the combine is a pure
+// stream and needs that memory-level parallelism.
 template <typename T, int MODE>
-__global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
+__device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
+                                            const cplx<T>* __restrict__ E,
+                                            const cplx<T>* __restrict__ P1,
+                                            const cplx<T>* __restrict__ P12,
+                                            const cplx<T>* __restrict__ P2,
+                                            cplx<T>* __restrict__ vh, cplx<T>* __restrict__ u,
+                                            T ds, int debug) {
+  using V = cplx<T>;
+  constexpr int U = 4;
+  const bool nl = debug & 2;
+  for (int p0 = threadIdx.x; p0 < n; p0 += U * blockDim.x) {
+    V b[U], o1[U], o2[U], o3[U], o4[U];
+    int sp[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int p = p0 + q * blockDim.x;
+      if (p < n) {
+        sp[q] = pidx(d, p);
+        b[q] = x[sp[q]];
+        if (MODE == RHO_STAGE1 && !nl) {
+          o1[q] = E[p]; o2[q] = vh[p]; o3[q] = P1[p]; o4[q] = P12[p];
+        } else if (MODE == RHO_STAGE2) {
+          o1[q] = P2[p]; o2[q] = u[p];
+        } else if (MODE == RHO_EULER) {
+          o1[q] = E[p]; o2[q] = vh[p]; o3[q] = P1[p];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int p = p0 + q * blockDim.x;
+      if (p >= n) continue;
+      const V bb = b[q];
+      if (MODE == RHO_STAGE1) {
+        if (nl) { o1[q] = bb; o2[q] = bb; o3[q] = bb; o4[q] = bb; }
+        const V ev = cmul(o1[q], o2[q]);
+        u[p] = cadd(ev, cmul(mk<V>(ds * o4[q].x, ds * o4[q].y), bb));
+        x[sp[q]] = cadd(ev, cmul(mk<V>(ds * o3[q].x, ds * o3[q].y), bb));
+      } else if (MODE == RHO_STAGE2) {
+        const V vn = cadd(o2[q], cmul(mk<V>(ds * o1[q].x, ds * o1[q].y), bb));
+        vh[p] = vn;
+        x[sp[q]] = vn;
+      } else if (MODE == RHO_EULER) {
+        const V vn = cadd(cmul(o1[q], o2[q]), cmul(mk<V>(ds * o3[q].x, ds * o3[q].y), bb));
+        vh[p] = vn;
+        x[sp[q]] = vn;
+      } else if (MODE == RHO_INIT) {
+        vh[p] = bb;
+      }
+    }
+  }
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(NWB_RHO_THREADS_LB, 1) k_rho(const RhoArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* x = reinterpret_cast<V*>(smem_raw);
@@ -213,38 +419,76 @@ __global__ void __launch_bounds__(512, 1) k_rho(const RhoArgs<T> a) {
     for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = x[pidx(a.dr, a.pos_r[f])];
     return;
   }
-  const T ds = a.ds;
-#pragma unroll 2
-  for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    const int sp = pidx(a.dr, p);
-    const V b = x[sp];
-    if (MODE == RHO_STAGE1) {
-      const bool nl = a.debug & 2;
-      const V e = nl ? b : a.E[trow + p], vh = nl ? b : a.vh[row + p];
-      const V p1 = nl ? b : a.P1[trow + p], p12 = nl ? b : a.P12[trow + p];
-      const V ev = cmul(e, vh);
-      const V vs = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), b));
-      a.u[row + p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), b));
-      x[sp] = vs;
-    } else if (MODE == RHO_STAGE2) {
-      const V p2 = a.P2[trow + p], u = a.u[row + p];
-      const V vn = cadd(u, cmul(mk<V>(ds * p2.x, ds * p2.y), b));
-      a.vh[row + p] = vn;
-      x[sp] = vn;
-    } else if (MODE == RHO_EULER) {
-      const V e = a.E[trow + p], vh = a.vh[row + p], p1 = a.P1[trow + p];
-      const V vn = cadd(cmul(e, vh), cmul(mk<V>(ds * p1.x, ds * p1.y), b));
-      a.vh[row + p] = vn;
-      x[sp] = vn;
-    } else if (MODE == RHO_INIT) {
-      a.vh[row + p] = b;
-    }
-  }
+  rho_combine<T, MODE>(x, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
+                       a.vh + row, a.u + row, a.ds, a.debug);
   __syncthreads();
   if (!(a.debug & 1)) fft_inverse(x, a.dr, 1, 0, a.tw_r);
   V* dst = a.out + row;
   for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+}
+
+// ------------------------------------------------------------------ rho pass, persistent
+// The march's rho pass as a persistent kernel: one CTA per SM walks columns
+// w = blockIdx.x, +gridDim.x, ...  A column's transform needs the whole column
+// in shared memory (176 KB at 10000 fp64 points), so an SM cannot hold a
+// second column to overlap with; L2 is used as the staging buffer instead.
+// While column w is transformed, its combine operands are already streaming
+// DRAM -> L2 (bulk prefetch issued with its load), and while w is inverse
+// transformed the next column's input is prefetched.  Consumed operands are
+// read and results written with evict-first hints so the staging does not
+// evict itself.
+
+template <typename V> __device__ __forceinline__ V ld_stream(const V* p) { return __ldcs(p); }
+template <typename V> __device__ __forceinline__ void st_stream(V* p, V v) { __stcs(p, v); }
+
+template <typename T, int MODE>
+__device__ __forceinline__ void prefetch_operands(const RhoArgs<T>& a, size_t row, size_t trow, int n) {
+  if (MODE == RHO_STAGE1) {
+    prefetch_row(a.vh + row, n);
+    prefetch_row(a.E + trow, n);
+    prefetch_row(a.P1 + trow, n);
+    prefetch_row(a.P12 + trow, n);
+  } else if (MODE == RHO_STAGE2) {
+    prefetch_row(a.u + row, n);
+    prefetch_row(a.P2 + trow, n);
+  } else if (MODE == RHO_EULER) {
+    prefetch_row(a.vh + row, n);
+    prefetch_row(a.E + trow, n);
+    prefetch_row(a.P1 + trow, n);
+  }
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(512, 1) k_rho_stream(const RhoArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* x = reinterpret_cast<V*>(smem_raw);
+  const int n = a.dr.n;
+  const int items = a.g.batch * a.g.kk;
+  for (int w = blockIdx.x; w < items; w += gridDim.x) {
+    const int mem = w % a.g.batch, k = w / a.g.batch;  // members of one mode adjacent: table reuse
+    const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+    const size_t trow = (size_t)k * a.g.ld;
+    const V* src = a.in + row;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &src[j]);
+    if (a.prefetch && threadIdx.x == 0) prefetch_operands<T, MODE>(a, row, trow, n);
+    cp_async_wait_all();
+    if (a.zero_bits && k == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
+    __syncthreads();
+    fft_forward(x, a.dr, 1, 0, a.tw_r);
+    rho_combine<T, MODE>(x, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
+                         a.vh + row, a.u + row, a.ds, 0);
+    const int wn = w + gridDim.x;
+    if (a.prefetch && threadIdx.x == 0 && wn < items)
+      prefetch_row(a.in + ((size_t)(wn % a.g.batch) * a.g.kk + wn / a.g.batch) * a.g.ld, n);
+    __syncthreads();
+    fft_inverse(x, a.dr, 1, 0, a.tw_r);
+    V* dst = a.out + row;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) st_stream(&dst[j], x[pidx(a.dr, j)]);
+    if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+    __syncthreads();  // smem is reloaded by the next column
+  }
 }
 
 // ------------------------------------------------------------------ rho pass, cluster split
@@ -298,31 +542,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2) k_rho_split(
   if (a.zero_bits && k == 0 && c == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
   __syncthreads();
   fft_forward(x, d2, 1, 0, a.tw_h2);
-  const T ds = a.ds;
-#pragma unroll 2
-  for (int p = threadIdx.x; p < h; p += blockDim.x) {
-    const int sp = pidx(d2, p);
-    const V b = x[sp];
-    if (MODE == RHO_STAGE1) {
-      const V e = a.E[htrow + p], vh = a.vh[hrow + p];
-      const V p1 = a.P1[htrow + p], p12 = a.P12[htrow + p];
-      const V ev = cmul(e, vh);
-      a.u[hrow + p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), b));
-      x[sp] = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), b));
-    } else if (MODE == RHO_STAGE2) {
-      const V p2 = a.P2[htrow + p], u = a.u[hrow + p];
-      const V vn = cadd(u, cmul(mk<V>(ds * p2.x, ds * p2.y), b));
-      a.vh[hrow + p] = vn;
-      x[sp] = vn;
-    } else if (MODE == RHO_EULER) {
-      const V e = a.E[htrow + p], vh = a.vh[hrow + p], p1 = a.P1[htrow + p];
-      const V vn = cadd(cmul(e, vh), cmul(mk<V>(ds * p1.x, ds * p1.y), b));
-      a.vh[hrow + p] = vn;
-      x[sp] = vn;
-    } else {  // RHO_INIT
-      a.vh[hrow + p] = b;
-    }
-  }
+  rho_combine<T, MODE>(x, d2, h, a.E + htrow, a.P1 + htrow, a.P12 + htrow, a.P2 + htrow,
+                       a.vh + hrow, a.u + hrow, a.ds, 0);
   __syncthreads();
   fft_inverse(x, d2, 1, 0, a.tw_h2);
   cluster.sync();  // both halves transformed and visible cluster-wide
@@ -447,8 +668,34 @@ static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
   k_theta_r2c<T, R><<<grid, 256, sm, s>>>(a);
 }
 
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename T, int R, bool C2R>
+static void theta_stream(const ThetaArgs<T>& a, cudaStream_t s) {
+  const size_t sm = 2 * (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
+  auto kern = C2R ? k_theta_c2r_stream<T, R> : k_theta_r2c_stream<T, R>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const long groups = (long)((a.g.nr + R - 1) / R) * a.g.batch;
+  const int ctas = (int)std::min<long>(groups, sm_count());
+  kern<<<ctas, 512, sm, s>>>(a);
+}
+
+// rows < 0 selects the persistent double-buffered kernel with R = -rows
 template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s) {
   switch (rows) {
+    case -1: theta_stream<T, 1, true>(a, s); break;
+    case -2: theta_stream<T, 2, true>(a, s); break;
+    case -4: theta_stream<T, 4, true>(a, s); break;
+    case -8: theta_stream<T, 8, true>(a, s); break;
     case 1: c2r_r<T, 1>(a, s); break;
     case 2: c2r_r<T, 2>(a, s); break;
     case 4: c2r_r<T, 4>(a, s); break;
@@ -457,6 +704,10 @@ template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cud
 }
 template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cudaStream_t s) {
   switch (rows) {
+    case -1: theta_stream<T, 1, false>(a, s); break;
+    case -2: theta_stream<T, 2, false>(a, s); break;
+    case -4: theta_stream<T, 4, false>(a, s); break;
+    case -8: theta_stream<T, 8, false>(a, s); break;
     case 1: r2c_r<T, 1>(a, s); break;
     case 2: r2c_r<T, 2>(a, s); break;
     case 4: r2c_r<T, 4>(a, s); break;
@@ -472,6 +723,18 @@ static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
       cudaFuncSetAttribute(k_rho_split<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       dim3 grid(2 * a.g.batch, a.g.kk);
       k_rho_split<T, MODE><<<grid, threads, sm, s>>>(a);
+      return;
+    }
+    if (a.persistent) {
+      const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);
+      cudaFuncSetAttribute(k_rho_stream<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      int dev = 0, sms = 148, occ = 1;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rho_stream<T, MODE>, threads, sm);
+      const long items = (long)a.g.batch * a.g.kk;
+      const long ctas = std::min<long>(items, (long)sms * (occ > 0 ? occ : 1));
+      k_rho_stream<T, MODE><<<(int)ctas, threads, sm, s>>>(a);
       return;
     }
   }

@@ -145,3 +145,90 @@ template void launch_tables<double>(const TableArgs&, double2*, double2*, double
 template void launch_tables<float>(const TableArgs&, float2*, float2*, float2*, float2*, double2*, cudaStream_t);
 
 }  // namespace nwb
+
+// ---------------------------------------------------------------- turbulence
+// Device port of the random-mode velocity field (reference
+// pkg/src/nwave/turbulence.py:145-203):
+//   a = kx_n lam sigma_i,  b = ky_n lam rho_j + phi_n
+//   c = cos a cos b - sin a sin b,  s = sin a cos b + cos a sin b
+//   U_par += amp1_n c, U_perp += amp2_n c, dU_perp/dsigma += w_ds_n s,
+//   dU_perp/drho += w_dr_n s,  modes accumulated in ascending order,
+// then scaled by 1/c0.  Same split and order as the reference's _mode_sum,
+// compiled without FMA contraction (this file), so the only difference is
+// the device's sincos (<= 1 ulp).
+
+namespace nwb {
+
+__global__ void k_mode_trig(const double* kx, const double* ky, const double* ph, double lam,
+                            const double* sig, int n_sig, const double* rho, int n_rho, int n_modes,
+                            double* ca, double* sa, double* cb, double* sb) {
+  const long tot_a = (long)n_sig * n_modes, tot_b = (long)n_modes * n_rho;
+  for (long t = blockIdx.x * (long)blockDim.x + threadIdx.x; t < tot_a + tot_b;
+       t += (long)gridDim.x * blockDim.x) {
+    if (t < tot_a) {
+      const int i = (int)(t / n_modes), n = (int)(t - (long)i * n_modes);
+      const double a = kx[n] * lam * sig[i];
+      double s, c;
+      sincos(a, &s, &c);
+      ca[t] = c;
+      sa[t] = s;
+    } else {
+      const long u = t - tot_a;
+      const int n = (int)(u / n_rho), j = (int)(u - (long)n * n_rho);
+      const double b = ky[n] * lam * rho[j] + ph[n];
+      double s, c;
+      sincos(b, &s, &c);
+      cb[u] = c;
+      sb[u] = s;
+    }
+  }
+}
+
+// one thread per (i, j); the mode loop walks the trig tables in order
+__global__ void k_mode_sum(int n_sig, int n_rho, int n_modes, const double* ca, const double* sa,
+                           const double* cb, const double* sb, const double* a1, const double* a2,
+                           const double* wds, const double* wdr, double inv_c0, double* u_par,
+                           double* u_perp, double* du_ds, double* du_dr) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= n_rho) return;
+  double up = 0, uq = 0, ds = 0, dr = 0;
+  const double* cai = ca + (size_t)i * n_modes;
+  const double* sai = sa + (size_t)i * n_modes;
+  for (int n = 0; n < n_modes; ++n) {
+    const double c_a = __ldg(cai + n), s_a = __ldg(sai + n);
+    const double c_b = cb[(size_t)n * n_rho + j], s_b = sb[(size_t)n * n_rho + j];
+    const double c = c_a * c_b - s_a * s_b;
+    const double s = s_a * c_b + c_a * s_b;
+    up += __ldg(a1 + n) * c;
+    uq += __ldg(a2 + n) * c;
+    ds += __ldg(wds + n) * s;
+    dr += __ldg(wdr + n) * s;
+  }
+  const size_t o = (size_t)i * n_rho + j;
+  u_par[o] = up * inv_c0;
+  u_perp[o] = uq * inv_c0;
+  du_ds[o] = ds * inv_c0;
+  du_dr[o] = dr * inv_c0;
+}
+
+void launch_turbulence(const double* kx, const double* ky, const double* ph, const double* a1,
+                       const double* a2, const double* wds, const double* wdr, int n_modes,
+                       double lam, double inv_c0, const double* sig, int n_sig, const double* rho,
+                       int n_rho, double* scratch, double* u_par, double* u_perp, double* du_ds,
+                       double* du_dr, cudaStream_t s) {
+  double* ca = scratch;
+  double* sa = ca + (size_t)n_sig * n_modes;
+  double* cb = sa + (size_t)n_sig * n_modes;
+  double* sb = cb + (size_t)n_modes * n_rho;
+  const long tot = (long)n_sig * n_modes + (long)n_modes * n_rho;
+  long blocks = (tot + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_mode_trig<<<(int)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(kx, ky, ph, lam, sig, n_sig, rho, n_rho,
+                                                            n_modes, ca, sa, cb, sb);
+  dim3 grid((n_rho + 127) / 128, n_sig);
+  k_mode_sum<<<grid, 128, 0, s>>>(n_sig, n_rho, n_modes, ca, sa, cb, sb, a1, a2, wds, wdr, inv_c0,
+                                  u_par, u_perp, du_ds, du_dr);
+}
+
+}  // namespace nwb

@@ -110,20 +110,25 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   const int rows = min(WT, nr - j0);
 
   // ---- theta faces, row by row: face f of a row lies between tile columns f-1 and f
+  // software-pipelined: row r+1 is loaded while row r's faces are computed
+  T v_lo = v[(size_t)j0 * nt + kl];
+  T v_hi = lane < 6 ? v[(size_t)j0 * nt + kh] : (T)0;
+  T c_cur = two_pi * upar[j0];
   for (int r = 0; r < rows; ++r) {
-    const int j = j0 + r;
-    const T c = two_pi * upar[j];
-    const T* vr = v + (size_t)j * nt;
-    T vv = vr[kl];
-    T g = -c * vv - hb * vv * vv, av = ath * vv;
+    T g = -c_cur * v_lo - hb * v_lo * v_lo, av = ath * v_lo;
     lpw[lane] = half * (g + av);
     lmw[lane] = half * (g - av);
     if (lane < 6) {
-      vv = vr[kh];
-      g = -c * vv - hb * vv * vv;
-      av = ath * vv;
+      g = -c_cur * v_hi - hb * v_hi * v_hi;
+      av = ath * v_hi;
       lpw[32 + lane] = half * (g + av);
       lmw[32 + lane] = half * (g - av);
+    }
+    if (r + 1 < rows) {
+      const T* vn = v + (size_t)(j0 + r + 1) * nt;
+      v_lo = vn[kl];
+      if (lane < 6) v_hi = vn[kh];
+      c_cur = two_pi * upar[j0 + r + 1];
     }
     __syncwarp();
     ftw[r][lane] = face_pair(lpw[lane], lpw[lane + 1], lpw[lane + 2], lpw[lane + 3], lpw[lane + 4],
@@ -163,11 +168,20 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   T fprev = (T)0;
   T* out = a.out + (size_t)mem * nr * nt;
   const bool col_ok = k < nt;
+  // software-pipelined: the value for window slot 5 of iteration r+1 is
+  // loaded while iteration r computes its face
+  int jn = wrap_idx(j0 + 2, nr);
+  T vnext = v[(size_t)jn * nt + kv];
+  T unext = uperp[jn];
   for (int r = 0; r <= rows; ++r) {
-    // load row j0 + r + 2 into window slot 5
-    const int jj = wrap_idx(j0 + r + 2, nr);
-    const T vv = v[(size_t)jj * nt + kv];
-    const T g = uperp[jj] * vv, av = arh * vv;
+    // row j0 + r + 2 into window slot 5
+    const T vv = vnext, uu = unext;
+    if (r < rows) {
+      jn = wrap_idx(j0 + r + 3, nr);
+      vnext = v[(size_t)jn * nt + kv];
+      unext = uperp[jn];
+    }
+    const T g = uu * vv, av = arh * vv;
     hp[5] = half * (g + av);
     hm[5] = half * (g - av);
     vw[5] = vv;

@@ -43,6 +43,8 @@ class VelocityFields:
         return self.u_par.shape
 
     def max_abs(self) -> float:
+        if hasattr(self.u_par, "abs"):  # device tensors
+            return float(max(self.u_par.abs().max(), self.u_perp.abs().max()))
         return float(max(np.max(np.abs(self.u_par)), np.max(np.abs(self.u_perp))))
 
 
@@ -155,6 +157,43 @@ def evaluate_fields(spec: TurbulenceSpec, lam: float, sigma_nodes,
         acc[3] += w_dr[n] * s
     inv_c0 = 1.0 / spec.c0
     return VelocityFields(*(a * inv_c0 for a in acc))
+
+
+def evaluate_fields_device(spec: TurbulenceSpec, lam: float, sigma_nodes, rho_nodes,
+                           device=None) -> VelocityFields:
+    """Device mode sum: the fields stay resident in HBM.
+
+    Same split, mode order and scaling as the host version and the reference
+    ``_mode_sum``; returns a ``VelocityFields`` of float64 CUDA tensors that
+    ``run_exprk22`` / ``DevicePlan.set_coeffs`` consume without a host round
+    trip (kernels ``k_mode_trig`` / ``k_mode_sum`` in csrc/tables.cu).
+    """
+    import torch
+
+    from . import _lib
+    from ._lib import check, ptr
+    from .plan import resolve_device
+
+    lib = _lib.lib()
+    dev = resolve_device(device)
+    lam = float(lam)
+    kx = spec.wavenumbers * np.cos(spec.angles)
+    ky = spec.wavenumbers * np.sin(spec.angles)
+    params = np.stack([kx, ky, spec.phases, spec.amp1, spec.amp2,
+                       -spec.amp2 * kx * lam, -spec.amp2 * ky * lam]).astype(np.float64)
+    n_modes = params.shape[1]
+    sig = np.ascontiguousarray(sigma_nodes, dtype=np.float64)
+    rho = np.ascontiguousarray(rho_nodes, dtype=np.float64)
+    with torch.cuda.device(dev):
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        p_d, s_d, r_d = t(params), t(sig), t(rho)
+        scratch = torch.empty(2 * (len(sig) + len(rho)) * n_modes, dtype=torch.float64, device=dev)
+        outs = [torch.empty((len(sig), len(rho)), dtype=torch.float64, device=dev) for _ in range(4)]
+        check(lib.nwb_turbulence_fields(n_modes, ptr(p_d), lam, 1.0 / spec.c0, ptr(s_d), len(sig),
+                                        ptr(r_d), len(rho), ptr(scratch), *(ptr(o) for o in outs),
+                                        torch.cuda.current_stream(dev).cuda_stream),
+              "nwb_turbulence_fields")
+    return VelocityFields(*outs)
 
 
 def downsample_fields(fields: VelocityFields, factor_sigma: int,

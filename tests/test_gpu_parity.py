@@ -341,3 +341,25 @@ def test_run_ensemble_members_match_single_runs(cuda, oracle):
         ref = oracle.march(cfg, v0s[m], f)
         assert max_relative(ref.final, res.final[i]) <= FP64_FIELD
         assert res.max_abs_v[i] == pytest.approx(ref.max_abs_v, abs=1e-12)
+
+
+def test_device_turbulence_generator_vs_reference(cuda, golden):
+    """device mode sum == reference evaluate_fields (golden)."""
+    c3 = nw.preset_config(1)
+    sig, _, _ = nw.build_axes(c3)
+    spec = nw.sample_modes(nw.TurbulenceParams(seed=0))
+    f = nw.turbulence.evaluate_fields_device(spec, spec.lam, sig[:5], nw.rho_nodes_closed(c3)[:33])
+    got = np.stack([t.cpu().numpy() for t in (f.u_par, f.u_perp, f.du_perp_dsigma, f.du_perp_drho)])
+    ref = golden["turb_small"]
+    assert np.max(np.abs(got - ref)) <= 1e-14 * np.max(np.abs(ref))
+
+
+def test_c3_with_device_medium(cuda, golden, golden_meta):
+    """C3 marched with coefficients generated and kept on the device."""
+    c3 = nw.preset_config(1)
+    sig, rho, theta = nw.build_axes(c3)
+    spec = nw.sample_modes(nw.TurbulenceParams(seed=0))
+    f = nw.turbulence.evaluate_fields_device(spec, spec.lam, sig, nw.rho_nodes_closed(c3))
+    rep = nw.run_exprk22(c3, nw.initial_nwave(rho, theta, c3.A, c3.B), f)
+    assert max_relative(golden["c3_double_final_sub"], rep.final.values[::8]) <= FP64_FIELD
+    assert abs(rep.max_abs_v - golden_meta["runs"]["c3_double"]["max_abs_v"]) <= 1e-12

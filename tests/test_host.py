@@ -174,5 +174,12 @@ def test_bench_roofline_bookkeeping():
     spec = cfg.N_rho * (cfg.N_theta // 2 + 1) * 16
     assert b[1] == 2 * F and b[3] == 7 * spec and b[7] == 5 * spec
     blk = bench.roofline_block(cfg, "c2", "double", [1.0, 2.0, 1.0, 3.0, 1.0, 2.0, 1.0, 2.5], 1)
-    assert blk["kernel"] == "weno" and blk["unit"] == "GB/s"
+    # both rho stages are one kernel (k_rho): 5.5 ms beats WENO's 4 ms
+    assert blk["kernel"] == "rho_pass" and blk["unit"] == "GB/s"
+    assert blk["achieved"] == pytest.approx((b[3] + b[7]) / 5.5e-3 / 1e9, rel=1e-3)
     assert 0 < blk["frac"] < 10
+    blk = bench.roofline_block(cfg, "c2", "double", [1.0, 4.0, 1.0, 1.0, 1.0, 4.0, 1.0, 1.0], 1)
+    assert blk["kernel"] == "weno"
+    # tables are shared by the members of a batch
+    b4 = bench.algorithmic_bytes(cfg, "double", 4)
+    assert b4[3] == 4 * 4 * spec + 3 * spec and b4[1] == 4 * 2 * F
