@@ -131,6 +131,37 @@ int nwb_weno5_b(int precision, int batch, int n_rho, int n_theta, const void* v_
                 double b_coef, double d_rho, double d_theta, void* out_dev,
                 void* workspace_dev, void* stream);
 
+/* ---- rho slabs: one large grid over G GPUs (BASELINE C5).
+ * A rank owns rho rows [j0, j0+rows) (physical / theta side) and theta modes
+ * [k0, k0+modes) (rho side).  Caller-owned buffers (device, working precision):
+ *   theta side: spec_rows (n_theta/2+1, ld_rows) complex, v_ext (rows+6, n_theta)
+ *               real with 3 halo rows above and below the owned rows, b (rows, n_theta)
+ *   rho side:   bt / out / vh / u (modes, ld_rho) complex (vh, u digit-reversed)
+ *   red: 2 x uint64 [alpha_theta bits, max|V| bits] (IEEE bits of non-negative
+ *        doubles: an integer MAX all-reduce across ranks is exact).
+ * The host performs the all-to-all between the layouts, the MAX all-reduce of
+ * red and the halo exchange (paper_2103_06080_b200/slab.py).  Modes of
+ * nwb_slab_rho: 0 stage 1, 1 stage 2, 2 exponential Euler, 3 init.
+ * These replace the same reference functions as nwb_march (exprk.py:151-331,
+ * weno.py:106-124) for a grid that does not fit one GPU. */
+typedef struct nwb_slab nwb_slab;
+int nwb_slab_create(nwb_slab** slab, int n_rho, int n_theta, int j0, int rows, int k0, int modes,
+                    int precision, double d_sigma, double rho_span, double theta_span, double A,
+                    double B, double eps, int device);
+int nwb_slab_destroy(nwb_slab* slab);
+int nwb_slab_set_stream(nwb_slab* slab, void* stream);
+int nwb_slab_layout(const nwb_slab* slab, int* ld_rows, int* ld_rho);
+int nwb_slab_set_coeffs(nwb_slab* slab, const double* u_par, const double* u_perp,
+                        const double* du_drho, int n_rows, int ld, int on_device);
+/* red == NULL: plain inverse transform (no reductions). */
+int nwb_slab_theta_c2r(nwb_slab* slab, const void* spec_rows_dev, void* v_ext_dev, int sigma_row,
+                       void* red_dev);
+int nwb_slab_weno(nwb_slab* slab, const void* v_ext_dev, void* b_dev, int sigma_row,
+                  const void* red_dev);
+int nwb_slab_theta_r2c(nwb_slab* slab, const void* b_dev, void* spec_rows_dev);
+int nwb_slab_rho(nwb_slab* slab, int mode, const void* bt_dev, void* out_dev, void* vh_dev,
+                 void* u_dev);
+
 /* Standalone multiplier tables in natural (n_rho, n_theta/2+1) layout; any
  * output may be NULL.  z is always complex128. */
 int nwb_tables(int precision, int n_rho, int n_theta, double rho_span, double theta_span,

@@ -35,7 +35,9 @@ ABI_SYMBOLS = (
     "nwb_plan_load_physical", "nwb_plan_load_spectrum", "nwb_plan_store_spectrum",
     "nwb_plan_store_physical", "nwb_march", "nwb_step", "nwb_rfft2", "nwb_irfft2",
     "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine", "nwb_profile_kernels",
-    "nwb_turbulence_fields",
+    "nwb_turbulence_fields", "nwb_slab_create", "nwb_slab_destroy", "nwb_slab_set_stream",
+    "nwb_slab_layout", "nwb_slab_set_coeffs", "nwb_slab_theta_c2r", "nwb_slab_weno",
+    "nwb_slab_theta_r2c", "nwb_slab_rho",
 )
 
 _lock = threading.Lock()
@@ -76,6 +78,18 @@ def _declare(lib):
                                c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p]),
         "nwb_phi": (c_int, [c_void_p, c_ll, c_int, c_void_p, c_void_p]),
+        "nwb_slab_create": (c_int, [P(c_void_p), c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                    c_double, c_double, c_double, c_double, c_double, c_double,
+                                    c_int]),
+        "nwb_slab_destroy": (c_int, [c_void_p]),
+        "nwb_slab_set_stream": (c_int, [c_void_p, c_void_p]),
+        "nwb_slab_layout": (c_int, [c_void_p, P(c_int), P(c_int)]),
+        "nwb_slab_set_coeffs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                        c_int]),
+        "nwb_slab_theta_c2r": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+        "nwb_slab_weno": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
+        "nwb_slab_theta_r2c": (c_int, [c_void_p, c_void_p, c_void_p]),
+        "nwb_slab_rho": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
         "nwb_turbulence_fields": (c_int, [c_int, c_void_p, c_double, c_double, c_void_p, c_int,
                                           c_void_p, c_int, c_void_p, c_void_p, c_void_p,
                                           c_void_p, c_void_p, c_void_p]),

@@ -833,7 +833,311 @@ int profile_impl(nwb_plan* p, int scheme, int n0, int n_steps, float* kernel_ms)
 
 }  // namespace
 
+// ====================================================================== rho slabs
+// Multi-GPU single-grid path (BASELINE config C5).  A rank owns
+// rho rows [j0, j0+rows) on the physical / theta side and theta modes
+// [k0, k0+modes) on the rho side; paper_2103_06080_b200/slab.py moves data
+// between the layouts (NCCL all-to-all), all-reduces alpha_theta / max|V|
+// and fills the 3-row WENO halos from the neighbouring ranks.  The state
+// buffers belong to the caller; the slab owns FFT plans, the multiplier
+// tables of its modes, and the (global) coefficient rows.
+
+struct nwb_slab {
+  int device = 0, prec = NWB_F64;
+  cudaStream_t stream = 0, own_stream = 0;
+  int nr = 0, nt = 0, m = 0, kk = 0;  // global grid
+  int j0 = 0, rows = 0, ld_rows = 0;  // owned rho rows (theta side)
+  int k0 = 0, modes = 0, ld_rho = 0;  // owned theta modes (rho side)
+  double d_sigma = 0, rho_span = 0, theta_span = 0, A = 0, B = 0, eps = 0;
+  FftDesc dr{}, dh{};
+  FftPlanHost plan_r, plan_h;
+  int rho_threads = 256;
+  void *tw_r = nullptr, *tw_h = nullptr, *wk = nullptr;
+  int *pos_r = nullptr, *rev_r = nullptr, *pos_h = nullptr;
+  void *E = nullptr, *P1 = nullptr, *P12 = nullptr, *P2 = nullptr;
+  void *upar = nullptr, *uperp = nullptr, *du = nullptr;
+  double* alpha_rho = nullptr;
+  int n_sig_rows = 0;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int salloc(nwb_slab* s, void** ptr, size_t bytes) {
+  cudaError_t e = cudaMallocAsync(ptr, bytes ? bytes : 16, s->stream);
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? NWB_ENOMEM : NWB_ECUDA,
+                std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+  }
+  s->allocs.push_back(*ptr);
+  return NWB_OK;
+}
+
+template <typename T> int slab_create_impl(nwb_slab* s) {
+  const size_t C = sizeof(cplx<T>);
+  std::vector<cplx<T>> twr, twh;
+  build_desc<T>(s->nr, s->plan_r, s->dr, twr);
+  build_desc<T>(s->m, s->plan_h, s->dh, twh);
+  auto wk = twiddles<T>(s->nt, s->kk);
+  auto fr = freq_of_pos(s->nr, s->plan_r.stages);
+  std::vector<int> pr(s->nr);
+  for (int q = 0; q < s->nr; ++q) pr[fr[q]] = q;
+  auto fh = freq_of_pos(s->m, s->plan_h.stages);
+  std::vector<int> ph(s->m);
+  for (int q = 0; q < s->m; ++q) ph[fh[q]] = q;
+  TRY(salloc(s, &s->tw_r, twr.size() * C));
+  TRY(salloc(s, &s->tw_h, twh.size() * C));
+  TRY(salloc(s, &s->wk, wk.size() * C));
+  TRY(salloc(s, (void**)&s->pos_r, pr.size() * sizeof(int)));
+  TRY(salloc(s, (void**)&s->rev_r, fr.size() * sizeof(int)));
+  TRY(salloc(s, (void**)&s->pos_h, ph.size() * sizeof(int)));
+  CU(cudaMemcpyAsync(s->tw_r, twr.data(), twr.size() * C, cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->tw_h, twh.data(), twh.size() * C, cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->wk, wk.data(), wk.size() * C, cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->pos_r, pr.data(), pr.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->rev_r, fr.data(), fr.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->pos_h, ph.data(), ph.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  const size_t tab = (size_t)s->modes * s->ld_rho * C;
+  for (void** t : {&s->E, &s->P1, &s->P12, &s->P2}) {
+    TRY(salloc(s, t, tab));
+    CU(cudaMemsetAsync(*t, 0, tab, s->stream));
+  }
+  TableArgs ta{};
+  ta.nr = s->nr; ta.nt = s->nt; ta.kk = s->modes; ta.ld = s->ld_rho; ta.k0 = s->k0;
+  ta.rho_span = s->rho_span; ta.theta_span = s->theta_span;
+  ta.d_sigma = s->d_sigma; ta.A = s->A; ta.eps = s->eps;
+  ta.rev_r = s->rev_r; ta.natural = 0;
+  launch_tables<T>(ta, (cplx<T>*)s->E, (cplx<T>*)s->P1, (cplx<T>*)s->P2, (cplx<T>*)s->P12,
+                   nullptr, s->stream);
+  CHECK_LAUNCH("slab tables");
+  CU(cudaStreamSynchronize(s->stream));  // host vectors above go out of scope
+  return NWB_OK;
+}
+
+template <typename T> int slab_coeffs_impl(nwb_slab* s, const double* up, const double* uq,
+                                           const double* du, int n_rows, int ld, int on_dev) {
+  const size_t n = (size_t)n_rows * s->nr;
+  for (void* a : {s->upar, s->uperp, s->du, (void*)s->alpha_rho})
+    if (a) cudaFreeAsync(a, s->stream);
+  TRY(salloc(s, &s->upar, n * sizeof(T)));
+  TRY(salloc(s, &s->uperp, n * sizeof(T)));
+  TRY(salloc(s, &s->du, n * sizeof(T)));
+  TRY(salloc(s, (void**)&s->alpha_rho, (size_t)n_rows * sizeof(double)));
+  double* stage = nullptr;
+  CU(cudaMallocAsync(&stage, n * sizeof(double), s->stream));
+  const double* srcs[3] = {up, uq, du};
+  void* dsts[3] = {s->upar, s->uperp, s->du};
+  for (int i = 0; i < 3; ++i) {
+    if (!srcs[i]) {
+      cudaMemsetAsync(dsts[i], 0, n * sizeof(T), s->stream);
+      continue;
+    }
+    cudaMemcpy2DAsync(stage, s->nr * sizeof(double), srcs[i], (size_t)ld * sizeof(double),
+                      s->nr * sizeof(double), n_rows,
+                      on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s->stream);
+    launch_convert<T>((long)n, stage, (T*)dsts[i], s->stream);
+  }
+  launch_alpha_rho<T>((const T*)s->uperp, s->nr, n_rows, s->alpha_rho, s->stream);
+  cudaFreeAsync(stage, s->stream);
+  s->n_sig_rows = n_rows;
+  CU(cudaStreamSynchronize(s->stream));
+  CHECK_LAUNCH("slab coeffs");
+  return NWB_OK;
+}
+
+template <typename T> ThetaArgs<T> slab_theta_args(const nwb_slab* s) {
+  ThetaArgs<T> a{};
+  a.g = Geom{s->rows, s->nt, s->m, s->kk, s->ld_rows, 1};
+  a.dh = s->dh;
+  a.tw_h = (const cplx<T>*)s->tw_h;
+  a.wk = (const cplx<T>*)s->wk;
+  a.pos_h = s->pos_h;
+  a.scale = (T)(1.0 / ((double)s->nr * (double)s->nt));
+  a.bcoef = (T)s->B;
+  a.coef_ld = s->nr;
+  a.coef_j0 = s->j0;
+  a.alpha_stride = 2;
+  a.vmax_stride = 2;
+  return a;
+}
+
+template <typename T> int slab_c2r_impl(nwb_slab* s, const void* spec, void* v_ext, int row, void* red) {
+  ThetaArgs<T> c = slab_theta_args<T>(s);
+  c.spec_in = (const cplx<T>*)spec;
+  c.phys_out = (T*)v_ext + (size_t)3 * s->nt;  // interior rows follow 3 halo rows
+  if (red) {
+    if (!s->upar) return fail(NWB_EINVAL, "coefficients not set");
+    c.upar = (const T*)s->upar;
+    c.row_off = row;
+    c.alpha_bits = (u64*)red;
+    c.vmax_bits = (u64*)red + 1;
+  }
+  launch_theta_c2r<T>(c, 1, s->stream);
+  CHECK_LAUNCH("slab c2r");
+  return NWB_OK;
+}
+
+template <typename T> int slab_weno_impl(nwb_slab* s, const void* v_ext, void* b, int row,
+                                         const void* red) {
+  if (!s->upar) return fail(NWB_EINVAL, "coefficients not set");
+  WenoArgs<T> w{};
+  w.g = Geom{s->rows, s->nt, s->m, s->kk, s->ld_rows, 1};
+  w.v = (const T*)v_ext;
+  w.out = (T*)b;
+  w.upar = (const T*)s->upar;
+  w.uperp = (const T*)s->uperp;
+  w.du = (const T*)s->du;
+  w.alpha_rho = s->alpha_rho;
+  w.row_off = row;
+  w.alpha_bits = (const u64*)red;
+  w.alpha_stride = 2;
+  w.bcoef = (T)s->B;
+  w.inv_drho = (T)(1.0 / (s->rho_span / s->nr));
+  w.inv_dtheta = (T)(1.0 / (s->theta_span / s->nt));
+  w.coef_ld = s->nr;
+  w.coef_j0 = s->j0;
+  w.nr_glob = s->nr;
+  w.halo = 1;
+  launch_weno<T>(w, s->stream);
+  CHECK_LAUNCH("slab weno");
+  return NWB_OK;
+}
+
+template <typename T> int slab_r2c_impl(nwb_slab* s, const void* b, void* spec) {
+  ThetaArgs<T> r = slab_theta_args<T>(s);
+  r.phys_in = (const T*)b;
+  r.spec_out = (cplx<T>*)spec;
+  launch_theta_r2c<T>(r, 1, s->stream);
+  CHECK_LAUNCH("slab r2c");
+  return NWB_OK;
+}
+
+template <typename T> int slab_rho_impl(nwb_slab* s, int mode, const void* bt, void* out, void* vh,
+                                        void* u) {
+  RhoArgs<T> q{};
+  q.g = Geom{s->nr, s->nt, s->m, s->modes, s->ld_rho, 1};
+  q.dr = s->dr;
+  q.tw_r = (const cplx<T>*)s->tw_r;
+  q.pos_r = s->pos_r;
+  q.in = (const cplx<T>*)bt;
+  q.out = (cplx<T>*)out;
+  q.vh = (cplx<T>*)vh;
+  q.u = (cplx<T>*)u;
+  q.E = (const cplx<T>*)s->E;
+  q.P1 = (const cplx<T>*)s->P1;
+  q.P12 = (const cplx<T>*)s->P12;
+  q.P2 = (const cplx<T>*)s->P2;
+  q.ds = (T)s->d_sigma;
+  q.prefetch = 1;
+  launch_rho<T>(q, mode, s->rho_threads, s->stream);
+  CHECK_LAUNCH("slab rho");
+  return NWB_OK;
+}
+
+}  // namespace
+
 // ====================================================================== C ABI
+
+int nwb_slab_create(nwb_slab** out, int n_rho, int n_theta, int j0, int rows, int k0, int modes,
+                    int precision, double d_sigma, double rho_span, double theta_span, double A,
+                    double B, double eps, int device) {
+  if (!out) return fail(NWB_EINVAL, "null slab pointer");
+  *out = nullptr;
+  if (precision != NWB_F64 && precision != NWB_F32) return fail(NWB_EINVAL, "unknown precision");
+  if (n_theta % 2) return fail(NWB_EUNSUPPORTED, "n_theta must be even");
+  const int kk = n_theta / 2 + 1;
+  if (rows < 1 || j0 < 0 || j0 + rows > n_rho || modes < 1 || k0 < 0 || k0 + modes > kk)
+    return fail(NWB_EINVAL, "slab ranges outside the grid");
+  nwb_slab* s = new nwb_slab();
+  s->device = device; s->prec = precision;
+  s->nr = n_rho; s->nt = n_theta; s->m = n_theta / 2; s->kk = kk;
+  s->j0 = j0; s->rows = rows; s->ld_rows = (rows + 7) / 8 * 8;
+  s->k0 = k0; s->modes = modes; s->ld_rho = (n_rho + 7) / 8 * 8;
+  s->d_sigma = d_sigma; s->rho_span = rho_span; s->theta_span = theta_span;
+  s->A = A; s->B = B; s->eps = eps;
+  if (!plan_fft(n_rho, false, s->plan_r) || !plan_fft(s->m, false, s->plan_h)) {
+    delete s;
+    return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
+  }
+  const int th = ((n_rho / 4) + 31) / 32 * 32;
+  s->rho_threads = th < 64 ? 64 : (th > 512 ? 512 : th);
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete s;
+    return fail(NWB_ECUDA, std::string("slab device/stream: ") + cudaGetErrorString(e));
+  }
+  s->stream = s->own_stream;
+  keep_pool_memory(device);
+  const int rc = precision == NWB_F64 ? slab_create_impl<double>(s) : slab_create_impl<float>(s);
+  if (rc != NWB_OK) {
+    nwb_slab_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return NWB_OK;
+}
+
+int nwb_slab_destroy(nwb_slab* s) {
+  if (!s) return NWB_OK;
+  cudaSetDevice(s->device);
+  cudaStreamSynchronize(s->stream);
+  for (void* a : s->allocs)
+    if (a) cudaFreeAsync(a, s->stream);
+  cudaStreamSynchronize(s->stream);
+  if (s->own_stream) cudaStreamDestroy(s->own_stream);
+  delete s;
+  return NWB_OK;
+}
+
+int nwb_slab_set_stream(nwb_slab* s, void* stream) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  s->stream = stream ? (cudaStream_t)stream : s->own_stream;
+  return NWB_OK;
+}
+
+int nwb_slab_layout(const nwb_slab* s, int* ld_rows, int* ld_rho) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (ld_rows) *ld_rows = s->ld_rows;
+  if (ld_rho) *ld_rho = s->ld_rho;
+  return NWB_OK;
+}
+
+int nwb_slab_set_coeffs(nwb_slab* s, const double* u_par, const double* u_perp,
+                        const double* du_drho, int n_rows, int ld, int on_device) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (n_rows < 1 || ld < s->nr) return fail(NWB_EINVAL, "coefficient rows / ld too small");
+  CU(cudaSetDevice(s->device));
+  return s->prec == NWB_F64 ? slab_coeffs_impl<double>(s, u_par, u_perp, du_drho, n_rows, ld, on_device)
+                            : slab_coeffs_impl<float>(s, u_par, u_perp, du_drho, n_rows, ld, on_device);
+}
+
+int nwb_slab_theta_c2r(nwb_slab* s, const void* spec, void* v_ext, int sigma_row, void* red) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (red && (sigma_row < 0 || sigma_row >= s->n_sig_rows)) return fail(NWB_EINVAL, "sigma row out of range");
+  return s->prec == NWB_F64 ? slab_c2r_impl<double>(s, spec, v_ext, sigma_row, red)
+                            : slab_c2r_impl<float>(s, spec, v_ext, sigma_row, red);
+}
+
+int nwb_slab_weno(nwb_slab* s, const void* v_ext, void* b, int sigma_row, const void* red) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (sigma_row < 0 || sigma_row >= s->n_sig_rows) return fail(NWB_EINVAL, "sigma row out of range");
+  return s->prec == NWB_F64 ? slab_weno_impl<double>(s, v_ext, b, sigma_row, red)
+                            : slab_weno_impl<float>(s, v_ext, b, sigma_row, red);
+}
+
+int nwb_slab_theta_r2c(nwb_slab* s, const void* b, void* spec) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  return s->prec == NWB_F64 ? slab_r2c_impl<double>(s, b, spec) : slab_r2c_impl<float>(s, b, spec);
+}
+
+int nwb_slab_rho(nwb_slab* s, int mode, const void* bt, void* out, void* vh, void* u) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (mode < RHO_STAGE1 || mode > RHO_INIT) return fail(NWB_EINVAL, "unknown rho mode");
+  return s->prec == NWB_F64 ? slab_rho_impl<double>(s, mode, bt, out, vh, u)
+                            : slab_rho_impl<float>(s, mode, bt, out, vh, u);
+}
 
 int nwb_profile_kernels(nwb_plan* p, int scheme, int n0, int n_steps, float* kernel_ms) {
   TRY(check_plan(p));

@@ -39,7 +39,8 @@ template <typename T> struct ThetaArgs {
   T* phys_out;
   T scale;                    // c2r output scale (1 / (nr nt))
   // optional reductions (c2r): alpha = max|2 pi u_par[j] + B v|, vmax = max|v|
-  const T* upar;              // coefficient table base (rows of nr) or null
+  const T* upar;              // coefficient table base (rows of coef_ld) or null
+  int coef_ld, coef_j0;       // coefficient row stride (0 = nr) and global row offset (slabs)
   const int* step_ctr;        // device step counter (row = *step_ctr + row_off) or null
   int row_off;
   T bcoef;
@@ -91,6 +92,9 @@ template <typename T> struct WenoArgs {
   int alpha_stride;
   T bcoef;
   T inv_drho, inv_dtheta;
+  // rho-slab mode (multi-GPU): coefficient row stride / global row offset /
+  // global row count, and v carrying 3 halo rows on each side (0 = plain)
+  int coef_ld, coef_j0, nr_glob, halo;
 };
 
 template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s);
@@ -119,6 +123,7 @@ struct TableArgs {
   double rho_span, theta_span, d_sigma, A, eps;
   const int* rev_r;           // position -> frequency (plan layout) or null (natural)
   int natural;                // 1: (nr, kk) row-major frequency order; 0: (kk, ld) digit-reversed
+  int k0;                     // first theta mode (theta-mode slab of a multi-GPU run)
 };
 template <typename T>
 void launch_tables(const TableArgs& a, cplx<T>* E, cplx<T>* P1, cplx<T>* P2, cplx<T>* P12,

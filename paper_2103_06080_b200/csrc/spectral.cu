@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const 
   fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
 
   const int step = a.step_ctr ? *a.step_ctr : 0;
-  const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * nr : nullptr;
+  const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * (a.coef_ld ? a.coef_ld : nr) + a.coef_j0 : nullptr;
   const T two_pi = (T)6.283185307179586476925;
   u64 amax = 0, vmax = 0;
   T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(512, 1) k_theta_c2r_stream(const ThetaArgs<T> 
     }
     __syncthreads();
     fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
-    const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * nr : nullptr;
+    const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * (a.coef_ld ? a.coef_ld : nr) + a.coef_j0 : nullptr;
     T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
     for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
       const int r = idx / m, n = idx - r * m, j = j0 + r;

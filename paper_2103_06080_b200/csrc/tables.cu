@@ -83,7 +83,7 @@ __global__ void k_tables(const TableArgs a, cplx<T>* E, cplx<T>* P1, cplx<T>* P2
     const int js = f <= (a.nr - 1) / 2 ? f : f - a.nr;                // fftfreq order
     const double jf = ((double)js * (1.0 / (double)a.nr)) * (double)a.nr;
     const double xi = two_pi * jf / a.rho_span;
-    const double om = two_pi * (double)k / a.theta_span;
+    const double om = two_pi * (double)(k + a.k0) / a.theta_span;
     const double2 den = make_double2(a.eps / (4.0 * pi), om);
     const double2 den4 = make_double2(4.0 * pi * den.x, 4.0 * pi * den.y);
     const double2 q = z_div(make_double2(-(xi * xi), 0.0), den4);

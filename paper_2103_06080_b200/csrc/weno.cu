@@ -93,15 +93,19 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   const int j0 = (blockIdx.y * WWARPS + w) * WT;
   if (j0 >= nr) return;  // warp-uniform
   const int row = (a.step_ctr ? *a.step_ctr : 0) + a.row_off;
-  const T* upar = a.upar + (size_t)row * nr;
-  const T* uperp = a.uperp + (size_t)row * nr;
-  const T* du = a.du + (size_t)row * nr;
+  // coefficient rows are global (rho slab: local row j is global cj0 + j)
+  const int cld = a.coef_ld ? a.coef_ld : nr, cj0 = a.coef_j0, ng = a.nr_glob ? a.nr_glob : nr;
+  const bool halo = a.halo != 0;  // slab mode: v holds 3 halo rows above and below
+  const T* upar = a.upar + (size_t)row * cld + cj0;
+  const T* uperp_g = a.uperp + (size_t)row * cld;
+  const T* du = a.du + (size_t)row * cld + cj0;
   const T ath = (T)bits_to_real(a.alpha_bits[(size_t)mem * a.alpha_stride]);
   const T arh = (T)a.alpha_rho[row];
   const T two_pi = (T)6.283185307179586476925;
   const T hb = (T)0.5 * a.bcoef;
   const T half = (T)0.5;
-  const T* v = a.v + (size_t)mem * nr * nt;
+  const T* v = a.v + (size_t)mem * (halo ? nr + 6 : nr) * nt;
+  auto vrow = [&](int jj) { return halo ? jj + 3 : wrap_idx(jj, nr); };
   T* lpw = lp[w];
   T* lmw = lm[w];
   T(*ftw)[WT + 1] = ft[w];
@@ -111,8 +115,8 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
 
   // ---- theta faces, row by row: face f of a row lies between tile columns f-1 and f
   // software-pipelined: row r+1 is loaded while row r's faces are computed
-  T v_lo = v[(size_t)j0 * nt + kl];
-  T v_hi = lane < 6 ? v[(size_t)j0 * nt + kh] : (T)0;
+  T v_lo = v[(size_t)vrow(j0) * nt + kl];
+  T v_hi = lane < 6 ? v[(size_t)vrow(j0) * nt + kh] : (T)0;
   T c_cur = two_pi * upar[j0];
   for (int r = 0; r < rows; ++r) {
     T g = -c_cur * v_lo - hb * v_lo * v_lo, av = ath * v_lo;
@@ -125,7 +129,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
       lmw[32 + lane] = half * (g - av);
     }
     if (r + 1 < rows) {
-      const T* vn = v + (size_t)(j0 + r + 1) * nt;
+      const T* vn = v + (size_t)vrow(j0 + r + 1) * nt;
       v_lo = vn[kl];
       if (lane < 6) v_hi = vn[kh];
       c_cur = two_pi * upar[j0 + r + 1];
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   if (lane < rows) {
     const int j = j0 + lane;
     const T c = two_pi * upar[j];
-    const T* vr = v + (size_t)j * nt;
+    const T* vr = v + (size_t)vrow(j) * nt;
     T p[6], m[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
@@ -158,9 +162,8 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   T hp[6], hm[6], vw[6];
 #pragma unroll
   for (int d = 0; d < 5; ++d) {
-    const int jj = wrap_idx(j0 - 3 + d, nr);
-    const T vv = v[(size_t)jj * nt + kv];
-    const T g = uperp[jj] * vv, av = arh * vv;
+    const T vv = v[(size_t)vrow(j0 - 3 + d) * nt + kv];
+    const T g = uperp_g[wrap_idx(cj0 + j0 - 3 + d, ng)] * vv, av = arh * vv;
     hp[d] = half * (g + av);
     hm[d] = half * (g - av);
     vw[d] = vv;
@@ -170,16 +173,14 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   const bool col_ok = k < nt;
   // software-pipelined: the value for window slot 5 of iteration r+1 is
   // loaded while iteration r computes its face
-  int jn = wrap_idx(j0 + 2, nr);
-  T vnext = v[(size_t)jn * nt + kv];
-  T unext = uperp[jn];
+  T vnext = v[(size_t)vrow(j0 + 2) * nt + kv];
+  T unext = uperp_g[wrap_idx(cj0 + j0 + 2, ng)];
   for (int r = 0; r <= rows; ++r) {
     // row j0 + r + 2 into window slot 5
     const T vv = vnext, uu = unext;
     if (r < rows) {
-      jn = wrap_idx(j0 + r + 3, nr);
-      vnext = v[(size_t)jn * nt + kv];
-      unext = uperp[jn];
+      vnext = v[(size_t)vrow(j0 + r + 3) * nt + kv];
+      unext = uperp_g[wrap_idx(cj0 + j0 + r + 3, ng)];
     }
     const T g = uu * vv, av = arh * vv;
     hp[5] = half * (g + av);
