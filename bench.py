@@ -329,6 +329,33 @@ def time_precision(cfg, cname, precision, steps, warmup, world, rank, local, clo
     return res
 
 
+def time_slab(cfg, steps, warmup, world, rank, local):
+    """C5: one grid split into rho slabs over the ranks (slab.py), fp64."""
+    import torch
+    from paper_2103_06080_b200.slab import SlabMarch
+
+    fields = coefficient_fields(cfg, "c5", warmup + steps + 2)
+    sm = SlabMarch(cfg, fields, device=torch.device("cuda", local),
+                   max_steps=warmup + steps + 1)
+    rows = sm.geo.rows()
+    sm.load(initial_field(cfg)[rows.start:rows.stop])
+    sm.march(n0=0, steps=warmup)
+    torch.cuda.synchronize(local)
+    barrier(world)
+    torch.cuda.synchronize(local)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local)
+    with sampler:
+        start.record()
+        sm.march(n0=warmup, steps=steps)
+        end.record()
+        torch.cuda.synchronize(local)
+    barrier(world)
+    ms = max_over_ranks(start.elapsed_time(end), world)
+    return {"value": cfg.N_rho * cfg.N_theta * steps / (ms * 1e-3), "ms_per_step": ms / steps,
+            "clocks": sampler.summary()}
+
+
 def e2e_precision(cfg, cname, precision, steps, world, rank, local):
     """Same metric through the public API with host buffers (run_exprk22)."""
     import torch
@@ -433,6 +460,18 @@ def main():
         return
 
     world, rank, local = dist_setup()
+    if args.config == "c5":
+        res = time_slab(cfg, args.steps, warmup, world, rank, local)
+        if rank == 0:
+            print(json.dumps({
+                "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {**config, "parallelism": f"rho-slab x{world} (all-to-all + halo)"},
+                "e2e": None, "gpu_launches": 8 * args.steps, "roofline": None,
+                "cpu_baseline": None, "clocks": res["clocks"], "impl": "b200"}), flush=True)
+        return
     res64 = time_precision(cfg, args.config, "double", args.steps, warmup, world, rank, local)
     res32 = None
     if not args.no_fp32:

@@ -276,8 +276,11 @@ class SlabMarch:
         self._theta_to_rho()
         o.rho(mode)
 
-    def march(self, scheme: str = "exprk22", guard: float = 10.0):
-        for n in range(self.n_steps):
+    def march(self, scheme: str = "exprk22", guard: float = 10.0, n0: int = 0,
+              steps: int | None = None):
+        """March ``steps`` steps from absolute step ``n0`` (default: the whole run)."""
+        stop = self.n_steps if steps is None else min(self.n_steps, n0 + steps)
+        for n in range(n0, stop):
             if scheme == "exprk22":
                 self._stage(n, RHO_STAGE1, True)
                 self._stage(n + 1, RHO_STAGE2, False)
