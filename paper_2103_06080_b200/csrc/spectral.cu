@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, 1) k_rho(const RhoArgs<T> 
       x[pidx(a.dr, p)] = val;
       if (a.vh) a.vh[row + p] = val;
     }
-  } else {
+  } else if (!(a.debug & 4)) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &src[j]);
     cp_async_wait_all();
   }
@@ -419,12 +419,15 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, 1) k_rho(const RhoArgs<T> 
     for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = x[pidx(a.dr, a.pos_r[f])];
     return;
   }
-  rho_combine<T, MODE>(x, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
-                       a.vh + row, a.u + row, a.ds, a.debug);
+  // debug bit 4 (measurement only): transforms without any global traffic
+  if (!(a.debug & 4))
+    rho_combine<T, MODE>(x, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
+                         a.vh + row, a.u + row, a.ds, a.debug);
   __syncthreads();
   if (!(a.debug & 1)) fft_inverse(x, a.dr, 1, 0, a.tw_r);
   V* dst = a.out + row;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
+  if (!(a.debug & 4))
+    for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
 }
 

@@ -16,7 +16,9 @@
 //    window of split fluxes -- one global load per cell, no transpose;
 //  * W() uses one reciprocal per face pair (common-denominator weights,
 //    w0 ~ 0.1 A1 A2, w1 ~ 0.6 A0 A2, w2 ~ 0.3 A0 A1 with A_i = (eps+beta_i)^2),
-//    SURVEY A.2 measured this reformulation at 1.2e-15 of the reference.
+//    SURVEY A.2 measured this reformulation at 1.2e-15 of the reference;
+//  * smoothness indicators scaled by 12 with eps folded into the centred
+//    second-difference term, which the rho sweep computes once per row.
 #include "internal.h"
 
 namespace nwb {
@@ -35,41 +37,64 @@ __device__ __forceinline__ double fast_rcp(double b) {
 }
 __device__ __forceinline__ float fast_rcp(float b) { return __frcp_rn(b); }
 
-// numerator / denominator of W(a0..a4) (reference _upwind_face) with
-// W = num / den
-template <typename T>
-__device__ __forceinline__ void face_nd(T a0, T a1, T a2, T a3, T a4, T& num, T& den) {
-  const T c1312 = (T)(13.0 / 12.0), q = (T)0.25, eps = (T)1e-6;
-  const T d0 = (a0 - (T)2 * a1) + a2, e0 = (a0 - (T)4 * a1) + (T)3 * a2;
-  const T d1 = (a1 - (T)2 * a2) + a3, e1 = a1 - a3;
-  const T d2 = (a2 - (T)2 * a3) + a4, e2 = ((T)3 * a2 - (T)4 * a3) + a4;
-  const T t0 = eps + (c1312 * (d0 * d0) + q * (e0 * e0));
-  const T t1 = eps + (c1312 * (d1 * d1) + q * (e1 * e1));
-  const T t2 = eps + (c1312 * (d2 * d2) + q * (e2 * e2));
-  const T A0 = t0 * t0, A1 = t1 * t1, A2 = t2 * t2;
-  const T w0 = (T)0.1 * (A1 * A2), w1 = (T)0.6 * (A0 * A2), w2 = (T)0.3 * (A0 * A1);
-  const T q0 = ((T)2 * a0 - (T)7 * a1) + (T)11 * a2;
-  const T q1 = (-a1 + (T)5 * a2) + (T)2 * a3;
-  const T q2 = ((T)2 * a2 + (T)5 * a3) - a4;
-  num = (w0 * q0 + w1 * q1) + w2 * q2;
-  den = (T)6 * ((w0 + w1) + w2);
+// Smoothness indicators scaled by 12 (the weights only depend on ratios):
+//   12 beta_i = 13 d_i^2 + 3 e_i^2,   d_i = centred second difference,
+// and the second-difference term D(c) = 13 d_c^2 depends only on the centre c,
+// so a sweep that owns consecutive centres computes each once (the rho sweep
+// keeps them in its register window).
+// (the 12 eps term is folded in here)
+template <typename T> __device__ __forceinline__ T dsq(T l, T c, T r) {
+  const T d = fma((T)-2, c, l) + r;
+  return fma((T)13 * d, d, (T)12e-6);
 }
 
-// F = W(p0..p4) + W(m0..m4) (m already in the reversed order of the source)
-__device__ __forceinline__ double face_pair(double p0, double p1, double p2, double p3, double p4,
-                                            double m0, double m1, double m2, double m3, double m4) {
-  double np, dp, nm, dm;
-  face_nd(p0, p1, p2, p3, p4, np, dp);
-  face_nd(m0, m1, m2, m3, m4, nm, dm);
-  // one reciprocal for both (fp64 range: den in [1e-24, 1e20])
-  return (np * dm + nm * dp) * fast_rcp(dp * dm);
+// numerator / denominator of W(a0..a4) (reference _upwind_face, weights
+// 0.1 : 0.6 : 0.3 -> 1 : 6 : 3 over common denominator A0 A1 A2) with
+// W = num / (6 den); D0..D2 = dsq at the centres a1, a2, a3
+//   num = A1 A2 q0 + A0 (6 A2 q1 + 3 A1 q2),  den = A1 A2 + A0 (6 A2 + 3 A1)
+template <typename T>
+__device__ __forceinline__ void face_nd(T a0, T a1, T a2, T a3, T a4, T D0, T D1, T D2, T& num,
+                                        T& den) {
+  const T e0 = fma((T)3, a2, fma((T)-4, a1, a0));
+  const T e1 = a1 - a3;
+  const T e2 = fma((T)3, a2, fma((T)-4, a3, a4));
+  const T t0 = fma((T)3 * e0, e0, D0);
+  const T t1 = fma((T)3 * e1, e1, D1);
+  const T t2 = fma((T)3 * e2, e2, D2);
+  const T A0 = t0 * t0, A1 = t1 * t1, A2 = t2 * t2;
+  const T q0 = fma((T)11, a2, fma((T)-7, a1, (T)2 * a0));
+  const T q1 = fma((T)2, a3, fma((T)5, a2, -a1));
+  const T q2 = fma((T)5, a3, fma((T)2, a2, -a4));
+  const T P = A1 * A2, x = (T)6 * A2, y = (T)3 * A1;
+  num = fma(A0, fma(x, q1, y * q2), P * q0);
+  den = fma(A0, x + y, P);
 }
-__device__ __forceinline__ float face_pair(float p0, float p1, float p2, float p3, float p4,
-                                           float m0, float m1, float m2, float m3, float m4) {
+
+// F = W(p0..p4) + W(m0..m4) (m already in the reversed order of the source),
+// second-difference terms supplied by the caller
+__device__ __forceinline__ double face_pair_d(double p0, double p1, double p2, double p3, double p4,
+                                              double Dp0, double Dp1, double Dp2, double m0,
+                                              double m1, double m2, double m3, double m4,
+                                              double Dm0, double Dm1, double Dm2) {
+  double np, dp, nm, dm;
+  face_nd(p0, p1, p2, p3, p4, Dp0, Dp1, Dp2, np, dp);
+  face_nd(m0, m1, m2, m3, m4, Dm0, Dm1, Dm2, nm, dm);
+  // one reciprocal for both (fp64 range of 6 dp dm: [1e-39, 1e19])
+  return (np * dm + nm * dp) * fast_rcp(6.0 * (dp * dm));
+}
+__device__ __forceinline__ float face_pair_d(float p0, float p1, float p2, float p3, float p4,
+                                             float Dp0, float Dp1, float Dp2, float m0, float m1,
+                                             float m2, float m3, float m4, float Dm0, float Dm1,
+                                             float Dm2) {
   float np, dp, nm, dm;
-  face_nd(p0, p1, p2, p3, p4, np, dp);
-  face_nd(m0, m1, m2, m3, m4, nm, dm);
-  return __fdividef(np, dp) + __fdividef(nm, dm);
+  face_nd(p0, p1, p2, p3, p4, Dp0, Dp1, Dp2, np, dp);
+  face_nd(m0, m1, m2, m3, m4, Dm0, Dm1, Dm2, nm, dm);
+  return __fdividef(np, 6.0f * dp) + __fdividef(nm, 6.0f * dm);
+}
+template <typename T>
+__device__ __forceinline__ T face_pair(T p0, T p1, T p2, T p3, T p4, T m0, T m1, T m2, T m3, T m4) {
+  return face_pair_d(p0, p1, p2, p3, p4, dsq(p0, p1, p2), dsq(p1, p2, p3), dsq(p2, p3, p4), m0, m1,
+                     m2, m3, m4, dsq(m0, m1, m2), dsq(m1, m2, m3), dsq(m2, m3, m4));
 }
 
 __device__ __forceinline__ int wrap_idx(int x, int n) {
@@ -101,9 +126,12 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   const T* du = a.du + (size_t)row * cld + cj0;
   const T ath = (T)bits_to_real(a.alpha_bits[(size_t)mem * a.alpha_stride]);
   const T arh = (T)a.alpha_rho[row];
-  const T two_pi = (T)6.283185307179586476925;
-  const T hb = (T)0.5 * a.bcoef;
+  const T pi = (T)3.14159265358979323846;
+  // split fluxes 0.5 (g +- alpha v) with g = -c v - (B/2) v^2 (theta) or
+  // u_perp v (rho), factored as v * (affine in v): 2 flops per split flux
+  const T qb = (T)-0.25 * a.bcoef;
   const T half = (T)0.5;
+  const T hath = half * ath, harh = half * arh;
   const T* v = a.v + (size_t)mem * (halo ? nr + 6 : nr) * nt;
   auto vrow = [&](int jj) { return halo ? jj + 3 : wrap_idx(jj, nr); };
   T* lpw = lp[w];
@@ -117,22 +145,20 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   // software-pipelined: row r+1 is loaded while row r's faces are computed
   T v_lo = v[(size_t)vrow(j0) * nt + kl];
   T v_hi = lane < 6 ? v[(size_t)vrow(j0) * nt + kh] : (T)0;
-  T c_cur = two_pi * upar[j0];
+  T c_cur = pi * upar[j0];
   for (int r = 0; r < rows; ++r) {
-    T g = -c_cur * v_lo - hb * v_lo * v_lo, av = ath * v_lo;
-    lpw[lane] = half * (g + av);
-    lmw[lane] = half * (g - av);
+    const T cp = hath - c_cur, cm = -hath - c_cur;  // c_cur = pi u_par
+    lpw[lane] = v_lo * fma(qb, v_lo, cp);
+    lmw[lane] = v_lo * fma(qb, v_lo, cm);
     if (lane < 6) {
-      g = -c_cur * v_hi - hb * v_hi * v_hi;
-      av = ath * v_hi;
-      lpw[32 + lane] = half * (g + av);
-      lmw[32 + lane] = half * (g - av);
+      lpw[32 + lane] = v_hi * fma(qb, v_hi, cp);
+      lmw[32 + lane] = v_hi * fma(qb, v_hi, cm);
     }
     if (r + 1 < rows) {
-      const T* vn = v + (size_t)vrow(j0 + r + 1) * nt;
+      const T* vn = v + (size_t)(halo ? j0 + r + 4 : j0 + r + 1) * nt;  // rows j0..j0+rows-1 < nr
       v_lo = vn[kl];
       if (lane < 6) v_hi = vn[kh];
-      c_cur = two_pi * upar[j0 + r + 1];
+      c_cur = pi * upar[j0 + r + 1];
     }
     __syncwarp();
     ftw[r][lane] = face_pair(lpw[lane], lpw[lane + 1], lpw[lane + 2], lpw[lane + 3], lpw[lane + 4],
@@ -142,15 +168,14 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   // 33rd theta face of row `lane` (between tile columns 31 and 32)
   if (lane < rows) {
     const int j = j0 + lane;
-    const T c = two_pi * upar[j];
+    const T cp = hath - pi * upar[j], cm = -hath - pi * upar[j];
     const T* vr = v + (size_t)vrow(j) * nt;
     T p[6], m[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
       const T vv = vr[wrap_idx(x0 + 29 + d, nt)];
-      const T g = -c * vv - hb * vv * vv, av = ath * vv;
-      p[d] = half * (g + av);
-      m[d] = half * (g - av);
+      p[d] = vv * fma(qb, vv, cp);
+      m[d] = vv * fma(qb, vv, cm);
     }
     ftw[lane][WT] = face_pair(p[0], p[1], p[2], p[3], p[4], m[5], m[4], m[3], m[2], m[1]);
   }
@@ -159,40 +184,65 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   // ---- rho sweep down column k with a register window of rows j-3 .. j+2
   const int k = x0 + lane;
   const int kv = wrap_idx(k, nt);
-  T hp[6], hm[6], vw[6];
+  // dp[s] / dm[s]: second-difference terms of hp / hm centred at window slot
+  // s (dp used at slots 1..3, dm at 2..4); each is computed once per row
+  T hp[6], hm[6], vw[6], dp[6], dm[6];
 #pragma unroll
   for (int d = 0; d < 5; ++d) {
     const T vv = v[(size_t)vrow(j0 - 3 + d) * nt + kv];
-    const T g = uperp_g[wrap_idx(cj0 + j0 - 3 + d, ng)] * vv, av = arh * vv;
-    hp[d] = half * (g + av);
-    hm[d] = half * (g - av);
+    const T uh = half * uperp_g[wrap_idx(cj0 + j0 - 3 + d, ng)];
+    hp[d] = vv * (uh + harh);
+    hm[d] = vv * (uh - harh);
     vw[d] = vv;
   }
+  dp[1] = dsq(hp[0], hp[1], hp[2]);
+  dp[2] = dsq(hp[1], hp[2], hp[3]);
+  dm[2] = dsq(hm[1], hm[2], hm[3]);
+  dm[3] = dsq(hm[2], hm[3], hm[4]);
   T fprev = (T)0;
-  T* out = a.out + (size_t)mem * nr * nt;
   const bool col_ok = k < nt;
+  // output / du pointers of row j0 (advanced one row per face after the first)
+  T* outp = a.out + (size_t)mem * nr * nt + (size_t)j0 * nt + (col_ok ? k : 0);
+  const T* dup = du + j0;
+  const T* ftp = &ftw[0][lane];
+  const T idth = a.inv_dtheta, idrh = a.inv_drho;
   // software-pipelined: the value for window slot 5 of iteration r+1 is
-  // loaded while iteration r computes its face
-  T vnext = v[(size_t)vrow(j0 + 2) * nt + kv];
-  T unext = uperp_g[wrap_idx(cj0 + j0 + 2, ng)];
+  // loaded while iteration r computes its face.  Running (wrapped) element
+  // offset / coefficient row of the prefetched row: they advance by one row
+  // per iteration, so the periodic wrap is a compare instead of a modulus.
+  const T* vcol = v + kv;
+  const int vwrap = (halo ? nr + 6 : nr) * nt;
+  int ov = vrow(j0 + 2) * nt, ju = wrap_idx(cj0 + j0 + 2, ng);
+  T vnext = vcol[ov];
+  T unext = uperp_g[ju];
+#pragma unroll 6
   for (int r = 0; r <= rows; ++r) {
     // row j0 + r + 2 into window slot 5
     const T vv = vnext, uu = unext;
     if (r < rows) {
-      vnext = v[(size_t)vrow(j0 + r + 3) * nt + kv];
-      unext = uperp_g[wrap_idx(cj0 + j0 + r + 3, ng)];
+      ov += nt;
+      ov = ov == vwrap ? 0 : ov;
+      ju = ju + 1 == ng ? 0 : ju + 1;
+      vnext = vcol[ov];
+      unext = uperp_g[ju];
     }
-    const T g = uu * vv, av = arh * vv;
-    hp[5] = half * (g + av);
-    hm[5] = half * (g - av);
+    hp[5] = vv * fma(half, uu, harh);
+    hm[5] = vv * fma(half, uu, -harh);
     vw[5] = vv;
+    dp[3] = dsq(hp[2], hp[3], hp[4]);
+    dm[4] = dsq(hm[3], hm[4], hm[5]);
     // face between rows j0+r-1 and j0+r
-    const T f = face_pair(hp[0], hp[1], hp[2], hp[3], hp[4], hm[5], hm[4], hm[3], hm[2], hm[1]);
-    if (r > 0 && col_ok) {
-      const int j = j0 + r - 1;
-      const T dth = (ftw[r - 1][lane + 1] - ftw[r - 1][lane]) * a.inv_dtheta;
-      const T drh = (f - fprev) * a.inv_drho;
-      out[(size_t)j * nt + k] = (du[j] * vw[2] - dth) - drh;
+    const T f = face_pair_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
+                            hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
+    if (r > 0) {
+      if (col_ok) {
+        const T dth = (ftp[1] - ftp[0]) * idth;
+        const T drh = (f - fprev) * idrh;
+        *outp = (*dup * vw[2] - dth) - drh;
+      }
+      outp += nt;
+      ++dup;
+      ftp += WT + 1;
     }
     fprev = f;
 #pragma unroll
@@ -200,6 +250,8 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
       hp[d] = hp[d + 1];
       hm[d] = hm[d + 1];
       vw[d] = vw[d + 1];
+      dp[d] = dp[d + 1];
+      dm[d] = dm[d + 1];
     }
   }
 }
