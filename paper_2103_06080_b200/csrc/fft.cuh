@@ -151,33 +151,71 @@ template <int RAD, bool INV, typename V> __device__ __forceinline__ void bfly(V*
   else bfly_odd<RAD, INV>(a);
 }
 
+// cos / sin (2 pi k / R) as compile-time constants (folded after unrolling):
+// quadrant reduction, then a Taylor series on [0, pi/4] (~1 ulp)
+__host__ __device__ constexpr double ce_sin_poly(double x) {
+  double x2 = x * x, term = x, s = x;
+  for (int k = 1; k < 12; ++k) {
+    term *= -x2 / ((2.0 * k) * (2.0 * k + 1.0));
+    s += term;
+  }
+  return s;
+}
+__host__ __device__ constexpr double ce_cos_poly(double x) {
+  double x2 = x * x, term = 1.0, s = 1.0;
+  for (int k = 1; k < 12; ++k) {
+    term *= -x2 / ((2.0 * k - 1.0) * (2.0 * k));
+    s += term;
+  }
+  return s;
+}
+// cos and sin of (pi/2) r / R for 0 <= r < R
+__host__ __device__ constexpr double ce_cos_q(int r, int R) {
+  return 2 * r <= R ? ce_cos_poly(1.57079632679489661923 * r / R)
+                    : ce_sin_poly(1.57079632679489661923 * (R - r) / R);
+}
+__host__ __device__ constexpr double ce_sin_q(int r, int R) {
+  return 2 * r <= R ? ce_sin_poly(1.57079632679489661923 * r / R)
+                    : ce_cos_poly(1.57079632679489661923 * (R - r) / R);
+}
+__host__ __device__ constexpr double ce_cos2pi(int k, int R) {
+  const int a = 4 * (k % R), q = a / R, r = a % R;
+  return q == 0 ? ce_cos_q(r, R) : q == 1 ? -ce_sin_q(r, R) : q == 2 ? -ce_cos_q(r, R) : ce_sin_q(r, R);
+}
+__host__ __device__ constexpr double ce_sin2pi(int k, int R) {
+  const int a = 4 * (k % R), q = a / R, r = a % R;
+  return q == 0 ? ce_sin_q(r, R) : q == 1 ? ce_cos_q(r, R) : q == 2 ? -ce_sin_q(r, R) : -ce_cos_q(r, R);
+}
+
+// v * W_R^k with W_R = exp(-2 pi i / R) (CONJ: exp(+2 pi i / R)); k known at
+// compile time after unrolling, the multiples of 1/8 turn are special-cased
+template <int R, bool CONJ, typename V> __device__ __forceinline__ V cmul_root(V v, int k) {
+  using S = decltype(V::x);
+  k %= R;
+  if (k == 0) return v;
+  if (2 * k == R) return mk<V>(-v.x, -v.y);
+  if (4 * k == R) return mul_i<CONJ>(v);           // W^k = -i (forward)
+  if (4 * k == 3 * R) return mul_i<!CONJ>(v);      // W^k = +i (forward)
+  const S c = (S)ce_cos2pi(k, R);
+  const S s = CONJ ? (S)ce_sin2pi(k, R) : -(S)ce_sin2pi(k, R);  // W^k = c + i s
+  if (8 * k == R || 8 * k == 3 * R || 8 * k == 5 * R || 8 * k == 7 * R) {
+    // |c| = |s| = 1/sqrt2: (x + iy)(c + is) with one product per component
+    return c == s ? mk<V>((v.x - v.y) * c, (v.x + v.y) * c) : mk<V>((v.x + v.y) * c, (v.y - v.x) * c);
+  }
+  return mk<V>(v.x * c - v.y * s, v.x * s + v.y * c);
+}
+
 // ------------------------------------------------------------ passes
 // A pass is one stage or two consecutive stages (ra then rb) fused in
 // registers: a thread loads the ra*rb elements {base + m s_a + n s_b}, runs
-// rb stage-a butterflies and ra stage-b butterflies, and writes back -- one
-// shared-memory round trip for two stages.  Twiddles come from per-stage
-// tables tw[off + (q-1) s + i] = W_L^{q i} (coalesced over i; the stage
-// tables of one transform total n - 1 entries).  Index math uses
-// multiply-high magic numbers (exact for x * d < 2^32, checked on the host).
+// them as one radix-(ra rb) butterfly (constant internal twiddles) and writes
+// back -- one shared-memory round trip for two stages.  The per-lane twiddle
+// W_L^i comes from a two-level table (coarse[i >> 6] * fine[i & 63]); its
+// powers are products.  Index math uses multiply-high magic numbers (exact
+// for x * d < 2^32, checked on the host).
 
 template <bool CONJ, typename V> __device__ __forceinline__ V twmul(V a, V w) {
   return CONJ ? cmulc(a, w) : cmul(a, w);
-}
-
-// t[q] *= W_L^{q i} (conjugated if CONJ), q = 1..R-1: W_L^i from the two-level
-// table (two L1-resident loads, one product), higher powers by products
-template <int R, bool CONJ, typename V>
-__device__ __forceinline__ void apply_tw(V* t, const V* __restrict__ coarse,
-                                         const V* __restrict__ fine, int i) {
-  if (i == 0) return;
-  const V w1 = cmul(__ldg(coarse + (i >> 6)), __ldg(fine + (i & 63)));
-  V w = w1;
-  t[1] = twmul<CONJ>(t[1], w);
-#pragma unroll
-  for (int q = 2; q < R; ++q) {
-    w = cmul(w, w1);
-    t[q] = twmul<CONJ>(t[q], w);
-  }
 }
 
 __device__ __forceinline__ unsigned fdiv(unsigned x, unsigned magic) {
@@ -197,9 +235,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
   const int per_row = nb * sb;
   const int total = per_row * rows;
   const V* twa = tw + d.pofs_a[p];
-  const V* twb = tw + d.pofs_b[p];
   const V* fia = tw + d.pfin_a[p];
-  const V* fib = tw + d.pfin_b[p];
   for (int g = threadIdx.x; g < total; g += blockDim.x) {
     const int row = (int)fdiv((unsigned)g, d.pmag_row[p]);
     const int h = g - row * per_row;
@@ -215,40 +251,61 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
 #pragma unroll
       for (int n2 = 0; n2 < RB; ++n2)
         a[m * RB + n2] = xr[fast ? pe0 + m * psa + n2 * psb : pidx(d, e0 + m * sa + n2 * sb)];
+    // The two stages form one radix-R butterfly (R = ra rb) on the elements
+    // i + (m rb + n2) s_b: stage a's twiddle W_L^{q (i + n2 s_b)} factors into
+    // W_L^{q i} (common to the n2 inputs of stage b's DFT, so it moves to the
+    // outputs) times the constant W_R^{q n2}; with stage b's W_{s_a}^{r i} =
+    // W_L^{ra r i} the output (q, r) twiddle is W_L^{(q + ra r) i}.  All R - 1
+    // output twiddles are powers of one W_L^i (two table loads, products in
+    // a log-depth tree) instead of one table lookup per stage and lane.
+    V pw[RA * RB];
+    {
+      pw[0] = mk<V>(1, 0);
+      if (RA * RB > 1) pw[1] = cmul(__ldg(twa + (i >> 6)), __ldg(fia + (i & 63)));
+#pragma unroll
+      for (int t = 2; t < RA * RB; ++t) pw[t] = cmul(pw[t >> 1], pw[t - (t >> 1)]);
+    }
     if (!DIT) {
-      // stage a over m (lane i + n2 sb of span L), twiddle after
+      // stage a over m (per n2), internal twiddles W_R^{q n2}
 #pragma unroll
       for (int n2 = 0; n2 < RB; ++n2) {
         V t[RA];
 #pragma unroll
         for (int m = 0; m < RA; ++m) t[m] = a[m * RB + n2];
         bfly<RA, CONJ>(t);
-        apply_tw<RA, CONJ>(t, twa, fia, i + n2 * sb);
 #pragma unroll
-        for (int q = 0; q < RA; ++q) a[q * RB + n2] = t[q];
+        for (int q = 0; q < RA; ++q) a[q * RB + n2] = cmul_root<RA * RB, CONJ>(t[q], q * n2);
       }
       if (RB > 1) {
-        // stage b over n2 within each stage-a output q (lane i of span sa)
+        // stage b over n2 within each stage-a output q
 #pragma unroll
         for (int q = 0; q < RA; ++q) {
           V t[RB];
 #pragma unroll
           for (int n2 = 0; n2 < RB; ++n2) t[n2] = a[q * RB + n2];
           bfly<RB, CONJ>(t);
-          apply_tw<RB, CONJ>(t, twb, fib, i);
 #pragma unroll
           for (int r = 0; r < RB; ++r) a[q * RB + r] = t[r];
         }
       }
+#pragma unroll
+      for (int q = 0; q < RA; ++q)
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (q + RA * r) a[q * RB + r] = twmul<CONJ>(a[q * RB + r], pw[q + RA * r]);
     } else {
-      // inverse: stage b first (DIT order), then stage a
+      // inverse: output twiddles first, then stage b, internal twiddles, stage a
+#pragma unroll
+      for (int q = 0; q < RA; ++q)
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (q + RA * r) a[q * RB + r] = twmul<CONJ>(a[q * RB + r], pw[q + RA * r]);
       if (RB > 1) {
 #pragma unroll
         for (int q = 0; q < RA; ++q) {
           V t[RB];
 #pragma unroll
           for (int r = 0; r < RB; ++r) t[r] = a[q * RB + r];
-          apply_tw<RB, CONJ>(t, twb, fib, i);
           bfly<RB, CONJ>(t);
 #pragma unroll
           for (int n2 = 0; n2 < RB; ++n2) a[q * RB + n2] = t[n2];
@@ -258,8 +315,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
       for (int n2 = 0; n2 < RB; ++n2) {
         V t[RA];
 #pragma unroll
-        for (int q = 0; q < RA; ++q) t[q] = a[q * RB + n2];
-        apply_tw<RA, CONJ>(t, twa, fia, i + n2 * sb);
+        for (int q = 0; q < RA; ++q) t[q] = cmul_root<RA * RB, CONJ>(a[q * RB + n2], q * n2);
         bfly<RA, CONJ>(t);
 #pragma unroll
         for (int m = 0; m < RA; ++m) a[m * RB + n2] = t[m];
