@@ -104,6 +104,56 @@ unsigned magic_for(int d) {
   return (unsigned)((((unsigned long long)1 << 32) + (unsigned long long)d - 1) / (unsigned long long)d);
 }
 
+// measurement knob: NWB_PAD=<P> overrides the smem padding period of the
+// transform of length NWB_PAD_N
+static int pad_env_n() {
+  const char* e = std::getenv("NWB_PAD_N");
+  return e ? std::atoi(e) : -1;
+}
+
+// simulated shared-memory wavefronts of all passes for padding period P
+// (lane g of a pass handles butterfly g; element e at slot e + e / P)
+static double pad_cost(int n, const FftPlanHost& h, int P) {
+  long waves = 0, ideal = 0;
+  int L = n;
+  for (auto& ps : h.passes) {
+    const int ra = ps.first, rb = ps.second, R = ra * rb;
+    const int sa = L / ra, sb = sa / rb, total = (n / L) * sb;
+    for (int w0 = 0; w0 < total; w0 += 32)
+      for (int k = 0; k < R; ++k)
+        for (int q = w0; q < std::min(w0 + 32, total); q += 8) {
+          int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
+          for (int g = q; g < std::min(q + 8, total); ++g) {
+            const int blk = g / sb, i = g - blk * sb;
+            const int e = blk * L + i + (k / rb) * sa + (k % rb) * sb;
+            const int slot = P ? e + e / P : e;
+            mx = std::max(mx, ++cnt[slot & 7]);
+          }
+          waves += mx;
+          ++ideal;
+        }
+    L /= R;
+  }
+  return ideal ? (double)waves / (double)ideal : 1.0;
+}
+
+static int choose_pad(int n, const FftPlanHost& h) {
+  std::vector<int> cand = {0};
+  for (int P = 8; P <= 256 && P < n; P += 8) cand.push_back(P);
+  const int last = h.passes.empty() ? 1 : h.passes.back().first * h.passes.back().second;
+  if (last % 2 == 0 && last < n) cand.push_back(last);
+  int best = 0;
+  double best_cost = 1e30;
+  for (int P : cand) {
+    const double c = pad_cost(n, h, P);
+    if (c < best_cost - 1e-9) {
+      best_cost = c;
+      best = P;
+    }
+  }
+  return best;
+}
+
 // device descriptor + per-stage twiddle tables W_L^{q i} laid out [q-1][i]
 template <typename T>
 void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& tw) {
@@ -146,10 +196,13 @@ void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& t
     d.pmag_sb[p] = magic_for(sb);
     st += rb > 1 ? 2 : 1;
   }
-  // pad the smem line every P elements, P = size of the last pass, when P is
-  // even (an odd unit-stride pass is already bank-conflict free)
-  const int P = d.np ? (h.passes.back().first * h.passes.back().second) : 1;
-  d.pad_period = (P % 2 == 0 && P < n) ? P : 0;
+  // pad the smem line every P elements: P is chosen by simulating the
+  // shared-memory wavefronts of every pass (16-byte accesses are served 8
+  // lanes at a time; a wavefront per distinct 16-byte bank group), over
+  // P = 0, multiples of 8 (which keep the unit-stride load / store loops
+  // conflict free) and the size of the last pass
+  d.pad_period = choose_pad(n, h);
+  if (const char* env = std::getenv(n == pad_env_n() ? "NWB_PAD" : "NWB_PAD_OTHER")) d.pad_period = std::atoi(env);
   if ((size_t)padded_len(n, d.pad_period) * sizeof(cplx<T>) > 227u * 1024u) d.pad_period = 0;
   d.pad_magic = d.pad_period ? magic_for(d.pad_period) : 0u;
   st = 0;
@@ -208,8 +261,9 @@ struct nwb_plan {
   int theta_rows = 1, rho_threads = 256;
   int theta_stream_rows = 0;  // R of the streaming theta kernels (0 = not used)
   int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
-  int rho_prefetch = 1;      // bulk L2 prefetch of combine operands (NWB_RHO_PREFETCH=0 disables)
-  int rho_debug = 0;         // NWB_RHO_DEBUG measurement knobs (never set in production)
+  int rho_prefetch = 0;      // bulk L2 prefetch of combine operands (NWB_RHO_PREFETCH overrides)
+  int rho_debug = 0;
+  int theta_debug = 0;       // NWB_THETA_DEBUG (never set in production)         // NWB_RHO_DEBUG measurement knobs (never set in production)
   int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
   FftDesc dh2{};             // half-column descriptor (split mode)
   void *tw_h2 = nullptr, *tw_split = nullptr;
@@ -288,6 +342,7 @@ template <typename T> ThetaArgs<T> theta_args(const nwb_plan* p) {
   a.bcoef = (T)p->B;
   a.alpha_stride = 4;
   a.vmax_stride = p->hist_len;
+  a.debug = p->theta_debug;
   return a;
 }
 
@@ -1189,8 +1244,12 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     p->rho_split = 0;
     if (const char* env = std::getenv("NWB_RHO_SPLIT"))
       p->rho_split = (env[0] == '1' && n_rho % 2 == 0 && n_rho >= 16) ? 1 : 0;
+    // bulk L2 prefetch of the combine operands: off (measured slower at Set 4
+    // in both precisions since the radix-R passes and two fp32 CTAs per SM)
+    p->rho_prefetch = 0;
     if (const char* env = std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = env[0] == '1';
     if (const char* env = std::getenv("NWB_RHO_DEBUG")) p->rho_debug = std::atoi(env);
+    if (const char* env = std::getenv("NWB_THETA_DEBUG")) p->theta_debug = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_PERSIST")) p->rho_persistent = env[0] == '1';
     if (p->rho_debug) p->rho_persistent = 0;  // the knobs live in k_rho
   }
@@ -1214,6 +1273,10 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
       p->theta_rows = r;
       break;
     }
+  if (const char* env = std::getenv("NWB_THETA_ROWS")) {  // measurement knob
+    const int r = std::atoi(env);
+    if ((r == 1 || r == 2 || r == 4 || r == 8) && (size_t)r * row_bytes <= 200 * 1024) p->theta_rows = r;
+  }
   int th = ((n_rho / 4) + 31) / 32 * 32;
   p->rho_threads = th < 64 ? 64 : (th > 512 ? 512 : th);
   if (p->rho_split) p->rho_threads = p->rho_threads > 256 ? 256 : p->rho_threads;

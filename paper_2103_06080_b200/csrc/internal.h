@@ -48,6 +48,7 @@ template <typename T> struct ThetaArgs {
   int alpha_stride;
   u64* vmax_bits;             // per member, stride vmax_stride, slot = *step_ctr, or null
   int vmax_stride;
+  int debug;                  // NWB_THETA_DEBUG measurement knobs (bit 4: no global traffic)
 };
 
 template <typename T> struct RhoArgs {

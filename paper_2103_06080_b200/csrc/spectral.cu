@@ -51,6 +51,12 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 #define NWB_RHO_THREADS_LB 512
 #endif
 template <typename T> constexpr int theta_min_blocks() { return sizeof(T) == 8 ? NWB_THETA_MINB64 : 3; }
+// an fp32 rho column (<= 113 KB) leaves room for a second CTA per SM, whose
+// loads then overlap this one's transforms
+#ifndef NWB_RHO_MINB32
+#define NWB_RHO_MINB32 2
+#endif
+template <typename T> constexpr int rho_min_blocks() { return sizeof(T) == 8 ? 1 : NWB_RHO_MINB32; }
 
 // ------------------------------------------------------------------ theta c2r
 // X[0..m] staged in natural order (Im of X[0], X[m] dropped as pocketfft's c2r
@@ -70,7 +76,7 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const 
   const int mem = blockIdx.y;
   const int j0 = blockIdx.x * R;
   const V* src = a.spec_in + (size_t)mem * kk * ld;
-  for (int idx = threadIdx.x; idx < kk * R; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < kk * R && !(a.debug & 4); idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
     V* slot = &z[r * rs + pidx(a.dh, k)];
     if (j < nr) cp_async_c(slot, &src[(size_t)k * ld + j]);
@@ -99,7 +105,7 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const 
   const T two_pi = (T)6.283185307179586476925;
   u64 amax = 0, vmax = 0;
   T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
-  for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < R * m && !(a.debug & 4); idx += blockDim.x) {
     const int r = idx / m, n = idx - r * m, j = j0 + r;
     if (j >= nr) continue;
     const V zz = z[r * rs + pidx(a.dh, a.pos_h[n])];
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const 
   const int j0 = blockIdx.x * R;
   const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
   const int rs = padded_len(m, a.dh.pad_period);
-  for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < R * m && !(a.debug & 4); idx += blockDim.x) {
     const int r = idx / m, n = idx - r * m, j = j0 + r;
     V* slot = &z[r * rs + pidx(a.dh, n)];
     if (j < nr) cp_async_c(slot, reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n));
@@ -145,7 +151,7 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const 
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
-  for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < npairs * R && !(a.debug & 4); idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
     if (j >= nr) continue;
     const V zk = z[r * rs + pidx(a.dh, a.pos_h[k])];
@@ -368,7 +374,7 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
 }
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(NWB_RHO_THREADS_LB, 1) k_rho(const RhoArgs<T> a) {
+__global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho(const RhoArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* x = reinterpret_cast<V*>(smem_raw);
