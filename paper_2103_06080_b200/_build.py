@@ -24,12 +24,17 @@ BUILD_DIR = os.path.join(os.path.dirname(HERE), "build", "nwb200")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
           "--expt-relaxed-constexpr", "-I", CSRC, "-I", INCLUDE]
-UNITS = {
-    "spectral.cu": [],
-    "weno.cu": [],
-    "capi.cu": [],
-    "tables.cu": ["-fmad=false"],
-}
+# (object, source, extra flags): spectral.cu is split by part and type so its
+# FFT instantiations compile in parallel
+UNITS = [
+    ("spectral_theta_f64", "spectral.cu", ["-DNWB_SPEC_PART=1", "-DNWB_SPEC_T=double"]),
+    ("spectral_theta_f32", "spectral.cu", ["-DNWB_SPEC_PART=1", "-DNWB_SPEC_T=float"]),
+    ("spectral_rho_f64", "spectral.cu", ["-DNWB_SPEC_PART=2", "-DNWB_SPEC_T=double"]),
+    ("spectral_rho_f32", "spectral.cu", ["-DNWB_SPEC_PART=2", "-DNWB_SPEC_T=float"]),
+    ("weno", "weno.cu", []),
+    ("capi", "capi.cu", []),
+    ("tables", "tables.cu", ["-fmad=false"]),
+]
 
 
 def nvcc() -> str:
@@ -62,15 +67,15 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
     os.makedirs(build_dir, exist_ok=True)
     objs = []
     procs = []
-    for unit, extra in UNITS.items():
-        obj = os.path.join(build_dir, unit.replace(".cu", ".o"))
+    for name, unit, extra in UNITS:
+        obj = os.path.join(build_dir, name + ".o")
         cmd = [nvcc(), *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c",
                os.path.join(CSRC, unit), "-o", obj]
         if ptxas_v:
             cmd += ["-Xptxas", "-v"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        procs.append((unit, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
+        procs.append((name, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                              text=True)))
         objs.append(obj)
     failed = []

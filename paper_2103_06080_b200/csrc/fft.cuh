@@ -231,8 +231,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
   const int L = d.pspan[p];
   const int sa = L / RA;            // stage-a span
   const int sb = sa / RB;           // lane range
-  const int nb = d.n / L;           // blocks per row
-  const int per_row = nb * sb;
+  const int per_row = d.n / (RA * RB);  // butterflies per row (constant divisor)
   const int total = per_row * rows;
   const V* twa = tw + d.pofs_a[p];
   const V* fia = tw + d.pfin_a[p];

@@ -65,14 +65,77 @@ template <typename T> constexpr int rho_min_blocks() { return sizeof(T) == 8 ? 1
 //   Z[m-k] = conj(Ze) + i conj(Zo)
 // an inverse m-point DIF (natural in, digit-reversed out), and
 //   v[2n] = Re z[pos(n)] * scale, v[2n+1] = Im z[pos(n)] * scale.
+//
+// The reductions use per-row extremes: for a fixed row j the LF speed
+// |fl(c_j + fl(B v))| is a composition of monotone rounded operations in v,
+// so its maximum over the row is attained at v = max_k V or v = min_k V --
+// evaluating it at the two extremes gives the per-element maximum bitwise,
+// and max|V| = max(|max V|, |min V|).  fmax/fmin drop NaNs, so NaNs are
+// flagged separately and reported as the NaN pattern 0x7ff..f (it sorts above
+// every finite and infinite value, like the per-element bit maximum did).
+
+template <typename T, int R>
+__device__ __forceinline__ void c2r_pre(cplx<T>* z, const ThetaArgs<T>& a, int rs) {
+  using V = cplx<T>;
+  const int m = a.g.m, npairs = m / 2 + 1;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    V* zr = z + r * rs;
+    for (int k = threadIdx.x; k < npairs; k += blockDim.x) {
+      const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
+      V xk = zr[sk];
+      V xm = zr[sm];
+      if (k == 0) { xk.y = 0; xm.y = 0; }
+      const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
+      const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), __ldg(&a.wk[k]));
+      zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
+      if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
+    }
+  }
+}
+
+// scale, store R rows (j0 + r < nr) and fold their reductions into amax / vmax
+template <typename T, int R>
+__device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a, int rs, int mem,
+                                         int j0, int step, u64& amax, u64& vmax) {
+  using V = cplx<T>;
+  const int m = a.g.m, nr = a.g.nr;
+  T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
+  const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * (a.coef_ld ? a.coef_ld : nr) + a.coef_j0 : nullptr;
+  const T two_pi = (T)6.283185307179586476925;
+  const T scale = a.scale, bco = a.bcoef;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = j0 + r;
+    if (j >= nr) break;
+    const V* zr = z + r * rs;
+    V* drow = reinterpret_cast<V*>(dst + (size_t)j * a.g.nt);
+    T hi = -INFINITY, lo = INFINITY;
+    bool nan = false;
+    for (int n = threadIdx.x; n < m; n += blockDim.x) {
+      const V zz = zr[pidx(a.dh, __ldg(&a.pos_h[n]))];
+      const T v0 = zz.x * scale, v1 = zz.y * scale;
+      drow[n] = mk<V>(v0, v1);
+      hi = fmax(hi, fmax(v0, v1));
+      lo = fmin(lo, fmin(v0, v1));
+      nan |= (v0 != v0) | (v1 != v1);
+    }
+    if (threadIdx.x < m) {
+      const T c = up ? two_pi * up[j] : (T)0;
+      amax = max(amax, max(abs_bits(c + bco * hi), abs_bits(c + bco * lo)));
+      vmax = max(vmax, max(abs_bits(hi), abs_bits(lo)));
+      if (nan) amax = vmax = 0x7fffffffffffffffULL;  // NaN, above every abs_bits value
+    }
+  }
+}
 
 template <typename T, int R>
 __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
-  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld, kk = a.g.kk;
-  const int rs = padded_len(m, a.dh.pad_period);  // smem row stride (holds X[0..m])
+  const int kk = a.g.kk, nr = a.g.nr, ld = a.g.ld;
+  const int rs = padded_len(a.g.m, a.dh.pad_period);  // smem row stride (holds X[0..m])
   const int mem = blockIdx.y;
   const int j0 = blockIdx.x * R;
   const V* src = a.spec_in + (size_t)mem * kk * ld;
@@ -84,39 +147,13 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const 
   }
   cp_async_wait_all();
   __syncthreads();
-  const int npairs = m / 2 + 1;
-  for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
-    const int r = idx / npairs, k = idx - r * npairs;
-    V* zr = z + r * rs;
-    const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
-    V xk = zr[sk];
-    V xm = zr[sm];
-    if (k == 0) { xk.y = 0; xm.y = 0; }
-    const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
-    const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), a.wk[k]);
-    zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
-    if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
-  }
+  c2r_pre<T, R>(z, a, rs);
   __syncthreads();
   fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
-
+  if (a.debug & 4) return;
   const int step = a.step_ctr ? *a.step_ctr : 0;
-  const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * (a.coef_ld ? a.coef_ld : nr) + a.coef_j0 : nullptr;
-  const T two_pi = (T)6.283185307179586476925;
   u64 amax = 0, vmax = 0;
-  T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
-  for (int idx = threadIdx.x; idx < R * m && !(a.debug & 4); idx += blockDim.x) {
-    const int r = idx / m, n = idx - r * m, j = j0 + r;
-    if (j >= nr) continue;
-    const V zz = z[r * rs + pidx(a.dh, a.pos_h[n])];
-    const T v0 = zz.x * a.scale, v1 = zz.y * a.scale;
-    *reinterpret_cast<V*>(dst + (size_t)j * a.g.nt + 2 * n) = mk<V>(v0, v1);
-    const T c = up ? two_pi * up[j] : (T)0;
-    u64 s0 = abs_bits(c + a.bcoef * v0), s1 = abs_bits(c + a.bcoef * v1);
-    u64 q0 = abs_bits(v0), q1 = abs_bits(v1);
-    amax = max(amax, max(s0, s1));
-    vmax = max(vmax, max(q0, q1));
-  }
+  c2r_post<T, R>(z, a, rs, mem, j0, step, amax, vmax);
   if (a.alpha_bits || a.vmax_bits) {
     block_max2<T>(amax, vmax,
                   a.alpha_bits ? a.alpha_bits + (size_t)mem * a.alpha_stride : nullptr,
@@ -130,35 +167,22 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const 
 //   X[k] = ze + W_nt^k zo,   X[m-k] = conj(ze - W_nt^k zo).
 
 template <typename T, int R>
-__global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const ThetaArgs<T> a) {
+__device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a, int rs, int mem,
+                                         int j0) {
   using V = cplx<T>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* z = reinterpret_cast<V*>(smem_raw);
   const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
-  const int mem = blockIdx.y;
-  const int j0 = blockIdx.x * R;
-  const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
-  const int rs = padded_len(m, a.dh.pad_period);
-  for (int idx = threadIdx.x; idx < R * m && !(a.debug & 4); idx += blockDim.x) {
-    const int r = idx / m, n = idx - r * m, j = j0 + r;
-    V* slot = &z[r * rs + pidx(a.dh, n)];
-    if (j < nr) cp_async_c(slot, reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n));
-    else *slot = mk<V>(0, 0);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  fft_forward(z, a.dh, R, rs, a.tw_h);
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
-  for (int idx = threadIdx.x; idx < npairs * R && !(a.debug & 4); idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
     if (j >= nr) continue;
-    const V zk = z[r * rs + pidx(a.dh, a.pos_h[k])];
-    const V zm = z[r * rs + pidx(a.dh, a.pos_h[k == 0 ? 0 : m - k])];
+    const V* zr = z + r * rs;
+    const V zk = zr[pidx(a.dh, __ldg(&a.pos_h[k]))];
+    const V zm = zr[pidx(a.dh, __ldg(&a.pos_h[k == 0 ? 0 : m - k]))];
     const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
     const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
-    const V wz = cmul(a.wk[k], zo);
+    const V wz = cmul(__ldg(&a.wk[k]), zo);
     dst[(size_t)k * ld + j] = cadd(ze, wz);
     if (2 * k != m) {
       const V d = csub(ze, wz);
@@ -167,13 +191,38 @@ __global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const 
   }
 }
 
+template <typename T, int R>
+__global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const ThetaArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* z = reinterpret_cast<V*>(smem_raw);
+  const int m = a.g.m, nr = a.g.nr;
+  const int mem = blockIdx.y;
+  const int j0 = blockIdx.x * R;
+  const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
+  const int rs = padded_len(m, a.dh.pad_period);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = j0 + r;
+    V* zr = z + r * rs;
+    const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
+    for (int n = threadIdx.x; n < m && !(a.debug & 4); n += blockDim.x) {
+      if (j < nr) cp_async_c(&zr[pidx(a.dh, n)], &srow[n]);
+      else zr[pidx(a.dh, n)] = mk<V>(0, 0);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  fft_forward(z, a.dh, R, rs, a.tw_h);
+  if (a.debug & 4) return;
+  r2c_post<T, R>(z, a, rs, mem, j0);
+}
+
 // ------------------------------------------------------------------ theta passes, streaming
-// Persistent, double-buffered variants used by the march: one CTA per SM walks
-// groups of R rows; the cp.async staging of group i+1 is in flight while group
-// i is transformed and stored, so global traffic never stalls on the
-// transform (the single-shot kernels above alternate load and compute phases
-// and sit at ~2 TB/s).  Reductions are accumulated per thread and flushed
-// with one block reduction per member.
+// Persistent, double-buffered variants (NWB_THETA_STREAM=1): one CTA per SM
+// walks groups of R rows; the cp.async staging of group i+1 is in flight
+// while group i is transformed and stored.  Reductions are accumulated per
+// thread and flushed with one block reduction per member.
 
 template <typename T, int R>
 __device__ __forceinline__ void c2r_issue(const ThetaArgs<T>& a, cplx<T>* z, int rs, int grp,
@@ -193,13 +242,11 @@ template <typename T, int R>
 __global__ void __launch_bounds__(512, 1) k_theta_c2r_stream(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int m = a.g.m, nr = a.g.nr;
-  const int rs = padded_len(m, a.dh.pad_period);
+  const int nr = a.g.nr;
+  const int rs = padded_len(a.g.m, a.dh.pad_period);
   V* buf[2] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + R * rs};
   const int gpm = (nr + R - 1) / R, groups = gpm * a.g.batch;
   const int step = a.step_ctr ? *a.step_ctr : 0;
-  const T two_pi = (T)6.283185307179586476925;
-  const int npairs = m / 2 + 1;
   int grp = blockIdx.x, it = 0;
   if (grp < groups) c2r_issue<T, R>(a, buf[0], rs, grp, gpm);
   cp_async_commit();
@@ -212,32 +259,10 @@ __global__ void __launch_bounds__(512, 1) k_theta_c2r_stream(const ThetaArgs<T> 
     cp_async_wait_1();
     __syncthreads();
     const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
-    for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
-      const int r = idx / npairs, k = idx - r * npairs;
-      V* zr = z + r * rs;
-      const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
-      V xk = zr[sk];
-      V xm = zr[sm];
-      if (k == 0) { xk.y = 0; xm.y = 0; }
-      const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
-      const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), a.wk[k]);
-      zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
-      if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
-    }
+    c2r_pre<T, R>(z, a, rs);
     __syncthreads();
     fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
-    const T* up = a.upar ? a.upar + (size_t)(step + a.row_off) * (a.coef_ld ? a.coef_ld : nr) + a.coef_j0 : nullptr;
-    T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
-    for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
-      const int r = idx / m, n = idx - r * m, j = j0 + r;
-      if (j >= nr) continue;
-      const V zz = z[r * rs + pidx(a.dh, a.pos_h[n])];
-      const T v0 = zz.x * a.scale, v1 = zz.y * a.scale;
-      *reinterpret_cast<V*>(dst + (size_t)j * a.g.nt + 2 * n) = mk<V>(v0, v1);
-      const T c = up ? two_pi * up[j] : (T)0;
-      amax = max(amax, max(abs_bits(c + a.bcoef * v0), abs_bits(c + a.bcoef * v1)));
-      vmax = max(vmax, max(abs_bits(v0), abs_bits(v1)));
-    }
+    c2r_post<T, R>(z, a, rs, mem, j0, step, amax, vmax);
     // flush the reductions when this CTA's next group belongs to another member
     const bool flush = nxt >= groups || nxt / gpm != mem;
     if (flush && (a.alpha_bits || a.vmax_bits)) {
@@ -258,11 +283,15 @@ __device__ __forceinline__ void r2c_issue(const ThetaArgs<T>& a, cplx<T>* z, int
   const int m = a.g.m;
   const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
   const T* src = a.phys_in + (size_t)mem * a.g.nr * a.g.nt;
-  for (int idx = threadIdx.x; idx < R * m; idx += blockDim.x) {
-    const int r = idx / m, n = idx - r * m, j = j0 + r;
-    V* slot = &z[r * rs + pidx(a.dh, n)];
-    if (j < a.g.nr) cp_async_c(slot, reinterpret_cast<const V*>(src + (size_t)j * a.g.nt + 2 * n));
-    else *slot = mk<V>(0, 0);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int j = j0 + r;
+    V* zr = z + r * rs;
+    const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
+    for (int n = threadIdx.x; n < m; n += blockDim.x) {
+      if (j < a.g.nr) cp_async_c(&zr[pidx(a.dh, n)], &srow[n]);
+      else zr[pidx(a.dh, n)] = mk<V>(0, 0);
+    }
   }
 }
 
@@ -270,12 +299,10 @@ template <typename T, int R>
 __global__ void __launch_bounds__(512, 1) k_theta_r2c_stream(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
-  const int rs = padded_len(m, a.dh.pad_period);
+  const int nr = a.g.nr;
+  const int rs = padded_len(a.g.m, a.dh.pad_period);
   V* buf[2] = {reinterpret_cast<V*>(smem_raw), reinterpret_cast<V*>(smem_raw) + R * rs};
   const int gpm = (nr + R - 1) / R, groups = gpm * a.g.batch;
-  const int npairs = m / 2 + 1;
-  const T half = (T)0.5;
   int grp = blockIdx.x, it = 0;
   if (grp < groups) r2c_issue<T, R>(a, buf[0], rs, grp, gpm);
   cp_async_commit();
@@ -288,21 +315,7 @@ __global__ void __launch_bounds__(512, 1) k_theta_r2c_stream(const ThetaArgs<T> 
     __syncthreads();
     fft_forward(z, a.dh, R, rs, a.tw_h);
     const int mem = grp / gpm, j0 = (grp - mem * gpm) * R;
-    V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
-    for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
-      const int r = idx % R, k = idx / R, j = j0 + r;
-      if (j >= nr) continue;
-      const V zk = z[r * rs + pidx(a.dh, a.pos_h[k])];
-      const V zm = z[r * rs + pidx(a.dh, a.pos_h[k == 0 ? 0 : m - k])];
-      const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
-      const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
-      const V wz = cmul(a.wk[k], zo);
-      dst[(size_t)k * ld + j] = cadd(ze, wz);
-      if (2 * k != m) {
-        const V d = csub(ze, wz);
-        dst[(size_t)(m - k) * ld + j] = mk<V>(d.x, -d.y);
-      }
-    }
+    r2c_post<T, R>(z, a, rs, mem, j0);
     __syncthreads();
   }
   cp_async_wait_0();
@@ -787,16 +800,34 @@ template <typename T> void launch_convert(long n, const double* in, T* out, cuda
   k_convert<T><<<grid_cap(n, 256), 256, 0, s>>>(n, in, out);
 }
 
-#define NWB_INST(T)                                                                            \
+// The library compiles this file once per (part, type) so the slow
+// instantiations build in parallel: -DNWB_SPEC_PART=1 theta passes and the
+// small helpers, 2 rho passes; -DNWB_SPEC_T=double|float.  Without the
+// defines everything is instantiated.
+#define NWB_INST_THETA(T)                                                                      \
   template void launch_theta_c2r<T>(const ThetaArgs<T>&, int, cudaStream_t);                   \
   template void launch_theta_r2c<T>(const ThetaArgs<T>&, int, cudaStream_t);                   \
-  template void launch_rho<T>(const RhoArgs<T>&, int, int, cudaStream_t);                      \
   template void launch_transpose<T>(const Geom&, const cplx<T>*, cplx<T>*, int, cudaStream_t); \
   template void launch_combine<T>(long, int, double, const cplx<T>*, const cplx<T>*,           \
                                   const cplx<T>*, const cplx<T>*, const cplx<T>*,              \
                                   const cplx<T>*, const cplx<T>*, cplx<T>*, cudaStream_t);     \
   template void launch_convert<T>(long, const double*, T*, cudaStream_t);
-NWB_INST(double)
-NWB_INST(float)
+#define NWB_INST_RHO(T) template void launch_rho<T>(const RhoArgs<T>&, int, int, cudaStream_t);
+#if !defined(NWB_SPEC_PART) || NWB_SPEC_PART == 1
+#ifdef NWB_SPEC_T
+NWB_INST_THETA(NWB_SPEC_T)
+#else
+NWB_INST_THETA(double)
+NWB_INST_THETA(float)
+#endif
+#endif
+#if !defined(NWB_SPEC_PART) || NWB_SPEC_PART == 2
+#ifdef NWB_SPEC_T
+NWB_INST_RHO(NWB_SPEC_T)
+#else
+NWB_INST_RHO(double)
+NWB_INST_RHO(float)
+#endif
+#endif
 
 }  // namespace nwb
