@@ -67,8 +67,17 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
     os.makedirs(build_dir, exist_ok=True)
     objs = []
     procs = []
+    headers = [d for d in _sources() if not d.endswith(".cu")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
     for name, unit, extra in UNITS:
         obj = os.path.join(build_dir, name + ".o")
+        objs.append(obj)
+        src = os.path.join(CSRC, unit)
+        # incremental: an object is reused when newer than its source and every header
+        # (experiment variants and forced builds recompile everything)
+        if (not force and not defines and out is None and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), newest_header)):
+            continue
         cmd = [nvcc(), *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines], "-c",
                os.path.join(CSRC, unit), "-o", obj]
         if ptxas_v:
@@ -77,7 +86,6 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
             print(" ".join(cmd), file=sys.stderr)
         procs.append((name, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                              text=True)))
-        objs.append(obj)
     failed = []
     for unit, p in procs:
         out, _ = p.communicate()

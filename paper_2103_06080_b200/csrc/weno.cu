@@ -17,7 +17,7 @@
 //  * W() uses one reciprocal per face pair (common-denominator weights,
 //    w0 ~ 0.1 A1 A2, w1 ~ 0.6 A0 A2, w2 ~ 0.3 A0 A1 with A_i = (eps+beta_i)^2),
 //    SURVEY A.2 measured this reformulation at 1.2e-15 of the reference;
-//  * smoothness indicators scaled by 12 with eps folded into the centred
+//  * smoothness indicators scaled by 4 with eps folded into the centred
 //    second-difference term, which the rho sweep computes once per row.
 #include "internal.h"
 
@@ -37,15 +37,14 @@ __device__ __forceinline__ double fast_rcp(double b) {
 }
 __device__ __forceinline__ float fast_rcp(float b) { return __frcp_rn(b); }
 
-// Smoothness indicators scaled by 12 (the weights only depend on ratios):
-//   12 beta_i = 13 d_i^2 + 3 e_i^2,   d_i = centred second difference,
-// and the second-difference term D(c) = 13 d_c^2 depends only on the centre c,
-// so a sweep that owns consecutive centres computes each once (the rho sweep
-// keeps them in its register window).
-// (the 12 eps term is folded in here)
+// Smoothness indicators scaled by 4 (the weights only depend on ratios):
+//   4 (eps + beta_i) = (13/3) d_i^2 + e_i^2 + 4 eps,   d_i = centred second
+// difference, and the second-difference term D(c) = (13/3) d_c^2 + 4 eps
+// depends only on the centre c, so a sweep that owns consecutive centres
+// computes each once (the rho sweep keeps them in its register window).
 template <typename T> __device__ __forceinline__ T dsq(T l, T c, T r) {
   const T d = fma((T)-2, c, l) + r;
-  return fma((T)13 * d, d, (T)12e-6);
+  return fma((T)(13.0 / 3.0) * d, d, (T)4e-6);
 }
 
 // numerator / denominator of W(a0..a4) (reference _upwind_face, weights
@@ -58,9 +57,9 @@ __device__ __forceinline__ void face_nd(T a0, T a1, T a2, T a3, T a4, T D0, T D1
   const T e0 = fma((T)3, a2, fma((T)-4, a1, a0));
   const T e1 = a1 - a3;
   const T e2 = fma((T)3, a2, fma((T)-4, a3, a4));
-  const T t0 = fma((T)3 * e0, e0, D0);
-  const T t1 = fma((T)3 * e1, e1, D1);
-  const T t2 = fma((T)3 * e2, e2, D2);
+  const T t0 = fma(e0, e0, D0);
+  const T t1 = fma(e1, e1, D1);
+  const T t2 = fma(e2, e2, D2);
   const T A0 = t0 * t0, A1 = t1 * t1, A2 = t2 * t2;
   const T q0 = fma((T)11, a2, fma((T)-7, a1, (T)2 * a0));
   const T q1 = fma((T)2, a3, fma((T)5, a2, -a1));
@@ -79,7 +78,7 @@ __device__ __forceinline__ double face_pair_d(double p0, double p1, double p2, d
   double np, dp, nm, dm;
   face_nd(p0, p1, p2, p3, p4, Dp0, Dp1, Dp2, np, dp);
   face_nd(m0, m1, m2, m3, m4, Dm0, Dm1, Dm2, nm, dm);
-  // one reciprocal for both (fp64 range of 6 dp dm: [1e-39, 1e19])
+  // one reciprocal for both (6 dp dm >= 6 (4e-6)^8 ~ 4e-43: normal in fp64)
   return (np * dm + nm * dp) * fast_rcp(6.0 * (dp * dm));
 }
 __device__ __forceinline__ float face_pair_d(float p0, float p1, float p2, float p3, float p4,
