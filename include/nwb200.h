@@ -177,6 +177,18 @@ int nwb_turbulence_fields(int n_modes, const double* mode_params_dev, double lam
                           int n_rho, double* scratch_dev, double* u_par_dev, double* u_perp_dev,
                           double* du_dsigma_dev, double* du_drho_dev, void* stream);
 
+/* Ground metrics of marched fields (builder metric of SURVEY
+ * 8(d), host definition paper_2103_06080_b200/analysis.py ground_metrics):
+ * for each member of v_dev (batch, n_rho, n_theta) in the working precision,
+ * on row `row` restricted to theta indices [k0, k1] with node values
+ * x_dev[0 .. k1-k0] (float64): out_dev[3 m + 0] = peak, [3 m + 1] = theta of
+ * the first upward crossing of 0.1 peak, [3 m + 2] = theta of the next upward
+ * crossing of 0.9 peak (NaN when absent), linearly interpolated, bitwise the
+ * host arithmetic.  Replaces the host post-processing of the reference CLI's
+ * snapshot path (cli.py:111-123 writes the field; the metric reads it). */
+int nwb_ground_metrics(int precision, int batch, int n_rho, int n_theta, const void* v_dev, int row,
+                       int k0, int k1, const double* x_dev, double* out_dev, void* stream);
+
 /* phi_shift(z) for complex128 z (shift 1 or 2). */
 int nwb_phi(const void* z_dev, long long n, int shift, void* out_dev, void* stream);
 /* Elementwise combines with numpy rounding (no FMA):

@@ -25,8 +25,12 @@ from .weno import weno5_b
 from .exprk import (EPS_DOUBLE, EPS_SINGLE, PhiMultipliers, SpectralTransforms,
                     build_multipliers, exp_euler_step, exprk22_step, phi1, phi2,
                     run_exprk22)
-from .analysis import (GRID_SETS, ensemble_nwaves, ground_metrics, initial_nwave,
-                       preset_config, rho_modulated)
+from .analysis import (GRID_SETS, GroundMetrics, ensemble_nwaves, ground_metrics,
+                       ground_metrics_device, initial_nwave, preset_config, rho_modulated)
+from .studies import (CheckpointComparison, ComparisonReport, ConvergenceRow, ScalingRow,
+                      TimingReport, compare_solvers, convergence_rate, convergence_study,
+                      cost_scaling_study, max_overshoot)
+from . import fieldio
 
 __all__ = [
     "BackendError", "BudgetExceededError", "CflViolationError", "ConfigError",
@@ -37,6 +41,8 @@ __all__ = [
     "zero_fields", "RunReport", "CflReport", "check_cfl_exprk", "check_cfl_splitting",
     "weno5_b", "EPS_DOUBLE", "EPS_SINGLE", "PhiMultipliers", "SpectralTransforms",
     "build_multipliers", "exp_euler_step", "exprk22_step", "phi1", "phi2", "run_exprk22",
-    "GRID_SETS", "ensemble_nwaves", "ground_metrics", "initial_nwave", "preset_config",
-    "rho_modulated",
+    "GRID_SETS", "GroundMetrics", "ensemble_nwaves", "ground_metrics", "ground_metrics_device",
+    "initial_nwave", "preset_config", "rho_modulated", "CheckpointComparison",
+    "ComparisonReport", "ConvergenceRow", "ScalingRow", "TimingReport", "compare_solvers",
+    "convergence_rate", "convergence_study", "cost_scaling_study", "max_overshoot", "fieldio",
 ]

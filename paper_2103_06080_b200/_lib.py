@@ -37,7 +37,7 @@ ABI_SYMBOLS = (
     "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine", "nwb_profile_kernels",
     "nwb_turbulence_fields", "nwb_slab_create", "nwb_slab_destroy", "nwb_slab_set_stream",
     "nwb_slab_layout", "nwb_slab_set_coeffs", "nwb_slab_theta_c2r", "nwb_slab_weno",
-    "nwb_slab_theta_r2c", "nwb_slab_rho",
+    "nwb_slab_theta_r2c", "nwb_slab_rho", "nwb_ground_metrics",
 )
 
 _lock = threading.Lock()
@@ -78,6 +78,8 @@ def _declare(lib):
                                c_double, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_void_p]),
         "nwb_phi": (c_int, [c_void_p, c_ll, c_int, c_void_p, c_void_p]),
+        "nwb_ground_metrics": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_int, c_int, c_int,
+                                       c_void_p, c_void_p, c_void_p]),
         "nwb_slab_create": (c_int, [P(c_void_p), c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                     c_double, c_double, c_double, c_double, c_double, c_double,
                                     c_int]),

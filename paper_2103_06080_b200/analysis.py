@@ -16,6 +16,7 @@
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -116,3 +117,37 @@ def ground_metrics(config: DomainConfig, field: Field2D, trace_rho: float = 144.
     t90 = _upward_crossing(y, x, 0.9 * peak, i10)
     rise = t90 - t10
     return GroundMetrics(float(rho[j]), peak, rise, rise * T0_SECONDS / (2.0 * np.pi))
+
+
+def ground_metrics_device(config: DomainConfig, v, trace_rho: float = 144.0,
+                          stream=None) -> list[GroundMetrics]:
+    """``ground_metrics`` of every member of a device field in one kernel
+    (``nwb_ground_metrics``): ``v`` is a CUDA tensor (batch, N_rho, N_theta) or
+    (N_rho, N_theta) in float64 or float32; only 3 doubles per member cross
+    to the host.  Bitwise the host definition above (same node values, same
+    rounded interpolation)."""
+    import torch
+
+    from . import _lib
+
+    if not (isinstance(v, torch.Tensor) and v.is_cuda):
+        raise TypeError("ground_metrics_device needs a CUDA tensor")
+    v = v.contiguous()
+    vb = v.reshape(-1, config.N_rho, config.N_theta)
+    prec = {torch.float64: _lib.F64, torch.float32: _lib.F32}.get(vb.dtype)
+    if prec is None:
+        raise TypeError(f"unsupported dtype {vb.dtype}")
+    _, rho, theta = build_axes(config)
+    j = int(round((trace_rho - config.rho_min) / config.d_rho))
+    k0, k1 = _index_range(theta, *config.roi_theta)
+    x = torch.as_tensor(theta[k0:k1 + 1], dtype=torch.float64, device=vb.device)
+    out = torch.empty((vb.shape[0], 3), dtype=torch.float64, device=vb.device)
+    lib = _lib.load_library()
+    s = stream if stream is not None else torch.cuda.current_stream(vb.device)
+    _lib.check(lib.nwb_ground_metrics(prec, vb.shape[0], config.N_rho, config.N_theta,
+                                      _lib.ptr(vb), j, k0, k1, _lib.ptr(x), _lib.ptr(out),
+                                      ctypes.c_void_p(s.cuda_stream)), "ground_metrics")
+    res = out.cpu().numpy()
+    return [GroundMetrics(float(rho[j]), float(pk), float(t90 - t10),
+                          float((t90 - t10) * T0_SECONDS / (2.0 * np.pi)))
+            for pk, t10, t90 in res]

@@ -259,6 +259,7 @@ struct nwb_plan {
   FftDesc dr{}, dh{};
   FftPlanHost plan_r, plan_h;
   int theta_rows = 1, rho_threads = 256;
+  int theta_rows_c2r = 1;    // c2r (transposed reads) favours many small CTAs for long rows
   int theta_stream_rows = 0;  // R of the streaming theta kernels (0 = not used)
   int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
   int rho_prefetch = 0;      // bulk L2 prefetch of combine operands (NWB_RHO_PREFETCH overrides)
@@ -403,7 +404,7 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   c.row_off = stage - 1;
   c.alpha_bits = p->red + (stage - 1);
   c.vmax_bits = stage == 1 ? p->vmax_hist : nullptr;
-  launch_theta_c2r<T>(c, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
+  launch_theta_c2r<T>(c, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows_c2r, s);
   if (ev) cudaEventRecord(ev[1], s);
   // WENO -> b
   WenoArgs<T> w = weno_args<T>(p);
@@ -647,7 +648,7 @@ template <typename T> int c2r_out(nwb_plan* p, const void* spec, void* out, doub
     c.vmax_bits = p->red + 2;  // slot 2 per member (stride 4, step 0)
     c.vmax_stride = 4;
   }
-  launch_theta_c2r<T>(c, p->theta_rows, p->stream);
+  launch_theta_c2r<T>(c, p->theta_rows_c2r, p->stream);
   CHECK_LAUNCH("c2r");
   if (max_abs) {
     std::vector<u64> h((size_t)p->g.batch * 4);
@@ -1277,6 +1278,14 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     const int r = std::atoi(env);
     if ((r == 1 || r == 2 || r == 4 || r == 8) && (size_t)r * row_bytes <= 200 * 1024) p->theta_rows = r;
   }
+  // c2r of long rows (>= 24 KB, e.g. fp64 Set 4): one-row 128-thread CTAs, four per
+  // SM in different phases, beat two-row CTAs (measured 0.234 vs 0.255 ms at C2);
+  // r2c keeps two rows (its transposed 16-byte stores would half-fill sectors)
+  p->theta_rows_c2r = row_bytes >= 24 * 1024 ? 1 : p->theta_rows;
+  if (const char* env = std::getenv("NWB_THETA_ROWS_C2R")) {  // measurement knob
+    const int r = std::atoi(env);
+    if ((r == 1 || r == 2 || r == 4 || r == 8) && (size_t)r * row_bytes <= 200 * 1024) p->theta_rows_c2r = r;
+  }
   int th = ((n_rho / 4) + 31) / 32 * 32;
   p->rho_threads = th < 64 ? 64 : (th > 512 ? 512 : th);
   if (p->rho_split) p->rho_threads = p->rho_threads > 256 ? 256 : p->rho_threads;
@@ -1428,6 +1437,24 @@ int nwb_turbulence_fields(int n_modes, const double* mode_params, double lam, do
                     rho_nodes, n_rho, scratch, u_par, u_perp, du_dsigma, du_drho,
                     (cudaStream_t)stream);
   CHECK_LAUNCH("turbulence");
+  return NWB_OK;
+}
+
+int nwb_ground_metrics(int precision, int batch, int n_rho, int n_theta, const void* v, int row,
+                       int k0, int k1, const double* x, double* out, void* stream) {
+  if (precision != NWB_F64 && precision != NWB_F32) return fail(NWB_EINVAL, "unknown precision");
+  if (batch < 1 || n_rho < 1 || n_theta < 1) return fail(NWB_EINVAL, "empty field");
+  if (row < 0 || row >= n_rho || k0 < 0 || k1 < k0 || k1 >= n_theta)
+    return fail(NWB_EINVAL, "ground row / roi outside the grid");
+  if (!v || !x || !out) return fail(NWB_EINVAL, "null buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (precision == NWB_F64)
+    launch_ground_metrics<double>((const double*)v, batch, n_rho, n_theta, row, k0, k1 - k0 + 1, x,
+                                  out, s);
+  else
+    launch_ground_metrics<float>((const float*)v, batch, n_rho, n_theta, row, k0, k1 - k0 + 1, x,
+                                 out, s);
+  CHECK_LAUNCH("ground_metrics");
   return NWB_OK;
 }
 

@@ -257,13 +257,26 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
     // W_L^{ra r i} the output (q, r) twiddle is W_L^{(q + ra r) i}.  All R - 1
     // output twiddles are powers of one W_L^i (two table loads, products in
     // a log-depth tree) instead of one table lookup per stage and lane.
-    V pw[RA * RB];
-    {
+    //
+    // The pass whose blocks are one butterfly (s_b = 1, the last DIF / first
+    // DIT pass) has i = 0: all its twiddles are 1 and are skipped (uniform
+    // branch).  The table loads are issued up front; the powers are formed
+    // next to their use so they are not live across the butterfly.
+    const bool tw_on = sb > 1;
+    V w1 = mk<V>(1, 0), w2 = mk<V>(0, 0);
+    if (tw_on) { w1 = __ldg(twa + (i >> 6)); w2 = __ldg(fia + (i & 63)); }
+    auto apply_tw = [&]() {
+      V pw[RA * RB];
       pw[0] = mk<V>(1, 0);
-      if (RA * RB > 1) pw[1] = cmul(__ldg(twa + (i >> 6)), __ldg(fia + (i & 63)));
+      pw[1] = cmul(w1, w2);
 #pragma unroll
       for (int t = 2; t < RA * RB; ++t) pw[t] = cmul(pw[t >> 1], pw[t - (t >> 1)]);
-    }
+#pragma unroll
+      for (int q = 0; q < RA; ++q)
+#pragma unroll
+        for (int r = 0; r < RB; ++r)
+          if (q + RA * r) a[q * RB + r] = twmul<CONJ>(a[q * RB + r], pw[q + RA * r]);
+    };
     if (!DIT) {
       // stage a over m (per n2), internal twiddles W_R^{q n2}
 #pragma unroll
@@ -287,18 +300,10 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
           for (int r = 0; r < RB; ++r) a[q * RB + r] = t[r];
         }
       }
-#pragma unroll
-      for (int q = 0; q < RA; ++q)
-#pragma unroll
-        for (int r = 0; r < RB; ++r)
-          if (q + RA * r) a[q * RB + r] = twmul<CONJ>(a[q * RB + r], pw[q + RA * r]);
+      if (RA * RB > 1 && tw_on) apply_tw();
     } else {
       // inverse: output twiddles first, then stage b, internal twiddles, stage a
-#pragma unroll
-      for (int q = 0; q < RA; ++q)
-#pragma unroll
-        for (int r = 0; r < RB; ++r)
-          if (q + RA * r) a[q * RB + r] = twmul<CONJ>(a[q * RB + r], pw[q + RA * r]);
+      if (RA * RB > 1 && tw_on) apply_tw();
       if (RB > 1) {
 #pragma unroll
         for (int q = 0; q < RA; ++q) {

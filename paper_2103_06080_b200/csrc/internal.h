@@ -116,6 +116,10 @@ void launch_combine(long n, int mode, double ds, const cplx<T>* E, const cplx<T>
                     const cplx<T>* b1, const cplx<T>* b2, cplx<T>* out, cudaStream_t s);
 template <typename T>
 void launch_convert(long n, const double* in, T* out, cudaStream_t s);
+// metrics.cu: per-member ground metrics (peak, t10, t90) of row `row`, roi [k0, k0+n)
+template <typename T>
+void launch_ground_metrics(const T* v, int batch, int nr, int nt, int row, int k0, int n,
+                           const double* x, double* out, cudaStream_t s);
 
 // tables.cu (compiled with -fmad=false so the z / exp / phi arithmetic
 // rounds like numpy's)

@@ -50,7 +50,12 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 #ifndef NWB_RHO_THREADS_LB
 #define NWB_RHO_THREADS_LB 512
 #endif
-template <typename T> constexpr int theta_min_blocks() { return sizeof(T) == 8 ? NWB_THETA_MINB64 : 3; }
+// threads per theta CTA: 128 per staged row up to 256 (one-row CTAs are
+// small, so more of them -- in different phases -- share an SM)
+template <int R> constexpr int theta_threads() { return R == 1 ? 128 : 256; }
+template <typename T, int R> constexpr int theta_min_blocks() {
+  return R == 1 ? (sizeof(T) == 8 ? 4 : 6) : (sizeof(T) == 8 ? NWB_THETA_MINB64 : 3);
+}
 // an fp32 rho column (<= 113 KB) leaves room for a second CTA per SM, whose
 // loads then overlap this one's transforms
 #ifndef NWB_RHO_MINB32
@@ -70,7 +75,7 @@ template <typename T> constexpr int rho_min_blocks() { return sizeof(T) == 8 ? 1
 // |fl(c_j + fl(B v))| is a composition of monotone rounded operations in v,
 // so its maximum over the row is attained at v = max_k V or v = min_k V --
 // evaluating it at the two extremes gives the per-element maximum bitwise,
-// and max|V| = max(|max V|, |min V|).  fmax/fmin drop NaNs, so NaNs are
+// and max|V| = max(|max V|, |min V|).  The compares skip NaNs, so NaNs are
 // flagged separately and reported as the NaN pattern 0x7ff..f (it sorts above
 // every finite and infinite value, like the per-element bit maximum did).
 
@@ -116,8 +121,11 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
       const V zz = zr[pidx(a.dh, __ldg(&a.pos_h[n]))];
       const T v0 = zz.x * scale, v1 = zz.y * scale;
       drow[n] = mk<V>(v0, v1);
-      hi = fmax(hi, fmax(v0, v1));
-      lo = fmin(lo, fmin(v0, v1));
+      // plain compares (NaNs are caught by the flag below)
+      const bool o = v0 > v1;
+      const T mx = o ? v0 : v1, mn = o ? v1 : v0;
+      hi = mx > hi ? mx : hi;
+      lo = mn < lo ? mn : lo;
       nan |= (v0 != v0) | (v1 != v1);
     }
     if (threadIdx.x < m) {
@@ -130,7 +138,7 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
 }
 
 template <typename T, int R>
-__global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_c2r(const ThetaArgs<T> a) {
+__global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())) k_theta_c2r(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
@@ -192,7 +200,7 @@ __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a
 }
 
 template <typename T, int R>
-__global__ void __launch_bounds__(256, theta_min_blocks<T>()) k_theta_r2c(const ThetaArgs<T> a) {
+__global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())) k_theta_r2c(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
@@ -680,14 +688,14 @@ static void c2r_r(const ThetaArgs<T>& a, cudaStream_t s) {
   const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_theta_c2r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
-  k_theta_c2r<T, R><<<grid, 256, sm, s>>>(a);
+  k_theta_c2r<T, R><<<grid, theta_threads<R>(), sm, s>>>(a);
 }
 template <typename T, int R>
 static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
   const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_theta_r2c<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
-  k_theta_r2c<T, R><<<grid, 256, sm, s>>>(a);
+  k_theta_r2c<T, R><<<grid, theta_threads<R>(), sm, s>>>(a);
 }
 
 static int sm_count() {

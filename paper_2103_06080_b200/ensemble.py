@@ -19,6 +19,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .analysis import ground_metrics_device
 from .errors import InstabilityError
 from .exprk import EPS_DOUBLE, EPS_SINGLE
 from .grid import DomainConfig
@@ -39,9 +40,10 @@ class EnsembleResult:
     members: range
     final: np.ndarray | None      # (n, N_rho, N_theta) float64, when keep_fields
     max_abs_v: np.ndarray         # per member, over all steps and the final field
-    peak: np.ndarray              # per member max_theta V at the ground trace row
+    peak: np.ndarray              # per member max_theta V over the roi of the ground trace row
     device_seconds: float
     n_steps: int
+    rise_theta: np.ndarray | None = None  # per member 10-90 % rise (theta units) at the trace row
 
 
 def run_ensemble(config: DomainConfig, v0s, fields, scheme: str = "exprk22",
@@ -81,13 +83,16 @@ def run_ensemble(config: DomainConfig, v0s, fields, scheme: str = "exprk22",
         v_fin, mx = plan.store_physical()
         torch.cuda.synchronize(plan.device)
         secs = time.perf_counter() - t0
-        j = int(round((trace_rho - config.rho_min) / config.d_rho)) % config.N_rho
-        peak = v_fin[:, j, :].max(dim=1).values.to("cpu", torch.float64).numpy()
+        # per-member ground metrics on the device (nwb_ground_metrics): only
+        # 3 doubles per member reach the host when the fields are not kept
+        gm = ground_metrics_device(config, v_fin, trace_rho, stream=plan.stream)
+        peak = np.array([g.peak for g in gm])
+        rise = np.array([g.rise_theta for g in gm])
         final = v_fin.to("cpu", torch.float64).numpy() if keep_fields else None
     finally:
         plan.close()
     mabs = np.maximum(max_abs.max(axis=1) if n_steps else 0.0, mx)
-    return EnsembleResult(members, final, mabs, peak, secs, n_steps)
+    return EnsembleResult(members, final, mabs, peak, secs, n_steps, rise)
 
 
 def gather_summaries(result: EnsembleResult, n_members: int, group=None):
