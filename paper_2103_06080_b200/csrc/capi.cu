@@ -253,6 +253,11 @@ struct nwb_plan {
   int device = 0;
   cudaStream_t stream = 0;
   cudaStream_t own_stream = 0;  // used when the caller sets none (graphs cannot capture the legacy stream)
+  // WENO / r2c overlap: the r2c of row chunk c runs on `side` while the WENO of
+  // chunk c+1 runs on `stream` (fork / join events; captured into the step graph)
+  int overlap_chunks = 0;
+  cudaStream_t side = 0;
+  cudaEvent_t ov_ev[9] = {};
   int prec = NWB_F64;
   Geom g{};
   double d_sigma = 0, rho_span = 0, theta_span = 0, A = 0, B = 0, eps = 0;
@@ -411,13 +416,33 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   w.step_ctr = p->step_ctr;
   w.row_off = stage - 1;
   w.alpha_bits = p->red + (stage - 1);
-  launch_weno<T>(w, s);
-  if (ev) cudaEventRecord(ev[2], s);
   // theta r2c of b -> bt
   ThetaArgs<T> r = theta_args<T>(p);
   r.phys_in = (const T*)p->b;
   r.spec_out = (cplx<T>*)p->bt;
-  launch_theta_r2c<T>(r, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
+  const int nc = p->overlap_chunks;
+  if (!ev && nc > 1 && !p->theta_stream_rows) {
+    // row chunks of 128-row multiples: WENO(c+1) on `s` overlaps r2c(c) on `side`
+    const int per = ((p->g.nr + nc - 1) / nc + 127) / 128 * 128;
+    int c = 0;
+    for (int j = 0; j < p->g.nr; j += per, ++c) {
+      const int je = j + per < p->g.nr ? j + per : p->g.nr;
+      w.row_begin = j;
+      w.row_end = je;
+      launch_weno<T>(w, s);
+      cudaEventRecord(p->ov_ev[c], s);
+      cudaStreamWaitEvent(p->side, p->ov_ev[c], 0);
+      r.row_begin = j;
+      r.row_end = je;
+      launch_theta_r2c<T>(r, p->theta_rows, p->side);
+    }
+    cudaEventRecord(p->ov_ev[8], p->side);
+    cudaStreamWaitEvent(s, p->ov_ev[8], 0);
+  } else {
+    launch_weno<T>(w, s);
+    if (ev) cudaEventRecord(ev[2], s);
+    launch_theta_r2c<T>(r, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
+  }
   if (ev) cudaEventRecord(ev[3], s);
   // rho pass
   RhoArgs<T> q = rho_args<T>(p);
@@ -1300,6 +1325,19 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     return fail(NWB_ECUDA, std::string("plan device/stream: ") + cudaGetErrorString(e));
   }
   p->stream = p->own_stream;
+  // WENO / r2c overlap chunks (NWB_OVERLAP=<chunks>, 0/1 = off; at most 8)
+  p->overlap_chunks = 0;
+  if (const char* env = std::getenv("NWB_OVERLAP")) p->overlap_chunks = std::atoi(env);
+  if (p->overlap_chunks > 8) p->overlap_chunks = 8;
+  if (p->overlap_chunks > 1) {
+    e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
+    for (int i = 0; i < 9 && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&p->ov_ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      nwb_plan_destroy(p);
+      return fail(NWB_ECUDA, std::string("overlap stream: ") + cudaGetErrorString(e));
+    }
+  }
   keep_pool_memory(device);
   int rc = precision == NWB_F64 ? create_impl<double>(p) : create_impl<float>(p);
   if (rc != NWB_OK) {
@@ -1319,6 +1357,9 @@ int nwb_plan_destroy(nwb_plan* p) {
   for (void* a : p->allocs)
     if (a) cudaFreeAsync(a, p->stream);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);
+  if (p->side) cudaStreamDestroy(p->side);
+  for (cudaEvent_t e : p->ov_ev)
+    if (e) cudaEventDestroy(e);
   delete p;
   return NWB_OK;
 }

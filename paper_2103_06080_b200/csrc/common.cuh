@@ -25,6 +25,30 @@ template <typename V> __device__ __forceinline__ V cmulc(V a, V b) {
 }
 template <typename V> __device__ __forceinline__ V cconj(V a) { return mk<V>(a.x, -a.y); }
 template <typename V> __device__ __forceinline__ V cscale(V a, decltype(V::x) s) { return mk<V>(a.x * s, a.y * s); }
+// acc + s * t (real s)
+template <typename V> __device__ __forceinline__ V caxpy(decltype(V::x) s, V t, V acc) {
+  return mk<V>(acc.x + s * t.x, acc.y + s * t.y);
+}
+
+// fp32 complex arithmetic on Blackwell's packed FP32 pipe: one (re, im) pair
+// is one float2 register pair, so adds are one FADD2 and a complex product is
+// FMUL2 + FFMA2 (sm_100: a plain FFMA issues half the FP32 peak).
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  return __ffma2_rn(b, make_float2(-1.0f, -1.0f), a);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  // (a.x b.x - a.y b.y, a.x b.y + a.y b.x)
+  return __ffma2_rn(make_float2(a.x, a.x), b, __fmul2_rn(make_float2(a.y, a.y), make_float2(-b.y, b.x)));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  // a conj(b) = (a.x b.x + a.y b.y, a.y b.x - a.x b.y)
+  return __ffma2_rn(make_float2(b.x, b.x), a, __fmul2_rn(make_float2(b.y, b.y), make_float2(a.y, -a.x)));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+__device__ __forceinline__ float2 caxpy(float s, float2 t, float2 acc) {
+  return __ffma2_rn(make_float2(s, s), t, acc);
+}
 // multiply by +i (INV=true) or -i (INV=false)
 template <bool PLUS, typename V> __device__ __forceinline__ V mul_i(V a) {
   return PLUS ? mk<V>(-a.y, a.x) : mk<V>(a.y, -a.x);

@@ -133,8 +133,8 @@ template <int RAD, bool INV, typename V> __device__ __forceinline__ void bfly_od
       const int m = (k * q) % RAD;
       const R cs = (R)odd_cos(RAD, m <= H ? m : RAD - m);
       const R sn = m <= H ? (R)odd_sin(RAD, m) : -(R)odd_sin(RAD, RAD - m);
-      bq = mk<V>(bq.x + cs * t[k].x, bq.y + cs * t[k].y);
-      cq = mk<V>(cq.x + sn * u[k].x, cq.y + sn * u[k].y);
+      bq = caxpy(cs, t[k], bq);
+      cq = caxpy(sn, u[k], cq);
     }
     // forward: y_q = b_q - i c_q, y_{r-q} = b_q + i c_q
     V ic = mul_i<true>(cq);
@@ -202,7 +202,7 @@ template <int R, bool CONJ, typename V> __device__ __forceinline__ V cmul_root(V
     // |c| = |s| = 1/sqrt2: (x + iy)(c + is) with one product per component
     return c == s ? mk<V>((v.x - v.y) * c, (v.x + v.y) * c) : mk<V>((v.x + v.y) * c, (v.y - v.x) * c);
   }
-  return mk<V>(v.x * c - v.y * s, v.x * s + v.y * c);
+  return cmul(v, mk<V>(c, s));
 }
 
 // ------------------------------------------------------------ passes

@@ -49,6 +49,9 @@ template <typename T> struct ThetaArgs {
   u64* vmax_bits;             // per member, stride vmax_stride, slot = *step_ctr, or null
   int vmax_stride;
   int debug;                  // NWB_THETA_DEBUG measurement knobs (bit 4: no global traffic)
+  // r2c row chunk [row_begin, row_end) (row_end 0 = all rows): the march overlaps
+  // the r2c of one chunk with the WENO of the next on a side stream
+  int row_begin, row_end;
 };
 
 template <typename T> struct RhoArgs {
@@ -96,6 +99,9 @@ template <typename T> struct WenoArgs {
   // rho-slab mode (multi-GPU): coefficient row stride / global row offset /
   // global row count, and v carrying 3 halo rows on each side (0 = plain)
   int coef_ld, coef_j0, nr_glob, halo;
+  // output row chunk [row_begin, row_end) (row_end 0 = all rows; row_begin a
+  // multiple of the CTA's 128 rows)
+  int row_begin, row_end;
 };
 
 template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s);

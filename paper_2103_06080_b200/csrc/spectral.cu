@@ -178,13 +178,14 @@ template <typename T, int R>
 __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a, int rs, int mem,
                                          int j0) {
   using V = cplx<T>;
-  const int m = a.g.m, nr = a.g.nr, ld = a.g.ld;
+  const int m = a.g.m, ld = a.g.ld;
+  const int jend = a.row_end ? a.row_end : a.g.nr;
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
   for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
-    if (j >= nr) continue;
+    if (j >= jend) continue;
     const V* zr = z + r * rs;
     const V zk = zr[pidx(a.dh, __ldg(&a.pos_h[k]))];
     const V zm = zr[pidx(a.dh, __ldg(&a.pos_h[k == 0 ? 0 : m - k]))];
@@ -205,8 +206,9 @@ __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
   const int m = a.g.m, nr = a.g.nr;
+  const int jend = a.row_end ? a.row_end : nr;
   const int mem = blockIdx.y;
-  const int j0 = blockIdx.x * R;
+  const int j0 = a.row_begin + blockIdx.x * R;
   const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
   const int rs = padded_len(m, a.dh.pad_period);
 #pragma unroll
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())
     V* zr = z + r * rs;
     const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
     for (int n = threadIdx.x; n < m && !(a.debug & 4); n += blockDim.x) {
-      if (j < nr) cp_async_c(&zr[pidx(a.dh, n)], &srow[n]);
+      if (j < jend) cp_async_c(&zr[pidx(a.dh, n)], &srow[n]);
       else zr[pidx(a.dh, n)] = mk<V>(0, 0);
     }
   }
@@ -694,7 +696,8 @@ template <typename T, int R>
 static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
   const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_theta_r2c<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
+  const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
+  dim3 grid((nrows + R - 1) / R, a.g.batch);
   k_theta_r2c<T, R><<<grid, theta_threads<R>(), sm, s>>>(a);
 }
 

@@ -19,6 +19,8 @@
 //    SURVEY A.2 measured this reformulation at 1.2e-15 of the reference;
 //  * smoothness indicators scaled by 4 with eps folded into the centred
 //    second-difference term, which the rho sweep computes once per row.
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace nwb {
@@ -114,8 +116,9 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mem = blockIdx.z;
   const int x0 = blockIdx.x * WT;
-  const int j0 = (blockIdx.y * WWARPS + w) * WT;
-  if (j0 >= nr) return;  // warp-uniform
+  const int jend = a.row_end ? a.row_end : nr;
+  const int j0 = a.row_begin + (blockIdx.y * WWARPS + w) * WT;
+  if (j0 >= jend) return;  // warp-uniform
   const int row = (a.step_ctr ? *a.step_ctr : 0) + a.row_off;
   // coefficient rows are global (rho slab: local row j is global cj0 + j)
   const int cld = a.coef_ld ? a.coef_ld : nr, cj0 = a.coef_j0, ng = a.nr_glob ? a.nr_glob : nr;
@@ -138,7 +141,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   T(*ftw)[WT + 1] = ft[w];
   const int kl = wrap_idx(x0 + lane - 3, nt);     // column loaded by this lane (line slot lane)
   const int kh = wrap_idx(x0 + lane + 29, nt);    // extra slot 32 + lane for lanes < 6
-  const int rows = min(WT, nr - j0);
+  const int rows = min(WT, jend - j0);
 
   // ---- theta faces, row by row: face f of a row lies between tile columns f-1 and f
   // software-pipelined: row r+1 is loaded while row r's faces are computed
@@ -255,6 +258,201 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
   }
 }
 
+// ------------------------------------------------------------------ fp32 on the packed pipe
+// Blackwell issues FP32 FMA at full rate only as FFMA2 (two lanes of a float2
+// per instruction); WENO in fp32 is issue-bound, so this variant gives each
+// lane TWO columns (k and k + 32 of a 64-column warp tile) and evaluates both
+// cells' faces with packed float2 arithmetic: the same formulas as k_weno
+// (face_nd / dsq are templates), half the FP instructions.
+
+struct f2 {
+  float2 v;
+  __device__ __forceinline__ f2() {}
+  __device__ __forceinline__ explicit f2(float s) : v(make_float2(s, s)) {}
+  __device__ __forceinline__ f2(float a, float b) : v(make_float2(a, b)) {}
+  __device__ __forceinline__ explicit f2(float2 x) : v(x) {}
+};
+__device__ __forceinline__ f2 operator+(f2 a, f2 b) { return f2(__fadd2_rn(a.v, b.v)); }
+__device__ __forceinline__ f2 operator*(f2 a, f2 b) { return f2(__fmul2_rn(a.v, b.v)); }
+__device__ __forceinline__ f2 operator-(f2 a) { return f2(-a.v.x, -a.v.y); }
+__device__ __forceinline__ f2 operator-(f2 a, f2 b) {
+  return f2(__ffma2_rn(b.v, make_float2(-1.0f, -1.0f), a.v));
+}
+__device__ __forceinline__ f2 fma(f2 a, f2 b, f2 c) { return f2(__ffma2_rn(a.v, b.v, c.v)); }
+using ::fma;  // keep the scalar overloads visible next to the packed one
+
+__device__ __forceinline__ f2 face_pair2(f2 p0, f2 p1, f2 p2, f2 p3, f2 p4, f2 m0, f2 m1, f2 m2,
+                                         f2 m3, f2 m4) {
+  f2 np, dp, nm, dm;
+  face_nd(p0, p1, p2, p3, p4, dsq(p0, p1, p2), dsq(p1, p2, p3), dsq(p2, p3, p4), np, dp);
+  face_nd(m0, m1, m2, m3, m4, dsq(m0, m1, m2), dsq(m1, m2, m3), dsq(m2, m3, m4), nm, dm);
+  const f2 d6p = f2(6.0f) * dp, d6m = f2(6.0f) * dm;
+  return f2(__fdividef(np.v.x, d6p.v.x) + __fdividef(nm.v.x, d6m.v.x),
+            __fdividef(np.v.y, d6p.v.y) + __fdividef(nm.v.y, d6m.v.y));
+}
+__device__ __forceinline__ f2 face_pair2_d(f2 p0, f2 p1, f2 p2, f2 p3, f2 p4, f2 Dp0, f2 Dp1,
+                                           f2 Dp2, f2 m0, f2 m1, f2 m2, f2 m3, f2 m4, f2 Dm0,
+                                           f2 Dm1, f2 Dm2) {
+  f2 np, dp, nm, dm;
+  face_nd(p0, p1, p2, p3, p4, Dp0, Dp1, Dp2, np, dp);
+  face_nd(m0, m1, m2, m3, m4, Dm0, Dm1, Dm2, nm, dm);
+  const f2 d6p = f2(6.0f) * dp, d6m = f2(6.0f) * dm;
+  return f2(__fdividef(np.v.x, d6p.v.x) + __fdividef(nm.v.x, d6m.v.x),
+            __fdividef(np.v.y, d6p.v.y) + __fdividef(nm.v.y, d6m.v.y));
+}
+
+constexpr int WT2 = 64;  // columns per warp tile (two per lane)
+
+__global__ void __launch_bounds__(WWARPS * 32) k_weno_f32x2(const WenoArgs<float> a) {
+  using T = float;
+  __shared__ T lp[WWARPS][WT2 + 8], lm[WWARPS][WT2 + 8];  // theta split fluxes of one row
+  __shared__ T ft[WWARPS][WT][WT2 + 1];                   // theta faces of the tile
+  const int nr = a.g.nr, nt = a.g.nt;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mem = blockIdx.z;
+  const int x0 = blockIdx.x * WT2;
+  const int jend = a.row_end ? a.row_end : nr;
+  const int j0 = a.row_begin + (blockIdx.y * WWARPS + w) * WT;
+  if (j0 >= jend) return;  // warp-uniform
+  const int row = (a.step_ctr ? *a.step_ctr : 0) + a.row_off;
+  const int cld = a.coef_ld ? a.coef_ld : nr, cj0 = a.coef_j0, ng = a.nr_glob ? a.nr_glob : nr;
+  const bool halo = a.halo != 0;
+  const T* upar = a.upar + (size_t)row * cld + cj0;
+  const T* uperp_g = a.uperp + (size_t)row * cld;
+  const T* du = a.du + (size_t)row * cld + cj0;
+  const T ath = (T)bits_to_real(a.alpha_bits[(size_t)mem * a.alpha_stride]);
+  const T arh = (T)a.alpha_rho[row];
+  const T pi = (T)3.14159265358979323846;
+  const T qb = (T)-0.25 * a.bcoef;
+  const T half = (T)0.5;
+  const T hath = half * ath, harh = half * arh;
+  const T* v = a.v + (size_t)mem * (halo ? nr + 6 : nr) * nt;
+  auto vrow = [&](int jj) { return halo ? jj + 3 : wrap_idx(jj, nr); };
+  T* lpw = lp[w];
+  T* lmw = lm[w];
+  T(*ftw)[WT2 + 1] = ft[w];
+  // line slot s holds column x0 + s - 3: lane loads slots lane, lane + 32, and
+  // lanes < 6 also slot 64 + lane
+  const int kl0 = wrap_idx(x0 + lane - 3, nt), kl1 = wrap_idx(x0 + lane + 29, nt);
+  const int kh = wrap_idx(x0 + lane + 61, nt);
+  const int rows = min(WT, jend - j0);
+
+  // ---- theta faces (faces lane and lane + 32 of each row, packed)
+  f2 vl(v[(size_t)vrow(j0) * nt + kl0], v[(size_t)vrow(j0) * nt + kl1]);
+  T v_hi = lane < 6 ? v[(size_t)vrow(j0) * nt + kh] : (T)0;
+  T c_cur = pi * upar[j0];
+  const f2 qb2(qb);
+  for (int r = 0; r < rows; ++r) {
+    const T cp = hath - c_cur, cm = -hath - c_cur;
+    const f2 sp = vl * fma(qb2, vl, f2(cp)), sm = vl * fma(qb2, vl, f2(cm));
+    lpw[lane] = sp.v.x;
+    lpw[lane + 32] = sp.v.y;
+    lmw[lane] = sm.v.x;
+    lmw[lane + 32] = sm.v.y;
+    if (lane < 6) {
+      lpw[64 + lane] = v_hi * fma(qb, v_hi, cp);
+      lmw[64 + lane] = v_hi * fma(qb, v_hi, cm);
+    }
+    if (r + 1 < rows) {
+      const T* vn = v + (size_t)(halo ? j0 + r + 4 : j0 + r + 1) * nt;
+      vl = f2(vn[kl0], vn[kl1]);
+      if (lane < 6) v_hi = vn[kh];
+      c_cur = pi * upar[j0 + r + 1];
+    }
+    __syncwarp();
+    auto P = [&](int d) { return f2(lpw[lane + d], lpw[lane + 32 + d]); };
+    auto M = [&](int d) { return f2(lmw[lane + d], lmw[lane + 32 + d]); };
+    const f2 fc = face_pair2(P(0), P(1), P(2), P(3), P(4), M(5), M(4), M(3), M(2), M(1));
+    ftw[r][lane] = fc.v.x;
+    ftw[r][lane + 32] = fc.v.y;
+    __syncwarp();
+  }
+  // 65th theta face of row `lane` (between tile columns 63 and 64), scalar
+  if (lane < rows) {
+    const int j = j0 + lane;
+    const T cp = hath - pi * upar[j], cm = -hath - pi * upar[j];
+    const T* vr = v + (size_t)vrow(j) * nt;
+    T p[6], m[6];
+#pragma unroll
+    for (int d = 0; d < 6; ++d) {
+      const T vv = vr[wrap_idx(x0 + 61 + d, nt)];
+      p[d] = vv * fma(qb, vv, cp);
+      m[d] = vv * fma(qb, vv, cm);
+    }
+    ftw[lane][WT2] = face_pair(p[0], p[1], p[2], p[3], p[4], m[5], m[4], m[3], m[2], m[1]);
+  }
+  __syncwarp();
+
+  // ---- rho sweep down columns k0 = x0 + lane and k1 = k0 + 32 (packed)
+  const int k0 = x0 + lane, k1 = k0 + 32;
+  const int kv0 = wrap_idx(k0, nt), kv1 = wrap_idx(k1, nt);
+  f2 hp[6], hm[6], vw[6], dp[6], dm[6];
+  const f2 harh2(harh), half2(half);
+#pragma unroll
+  for (int d = 0; d < 5; ++d) {
+    const size_t ro = (size_t)vrow(j0 - 3 + d) * nt;
+    const f2 vv(v[ro + kv0], v[ro + kv1]);
+    const f2 uh(half * uperp_g[wrap_idx(cj0 + j0 - 3 + d, ng)]);
+    hp[d] = vv * (uh + harh2);
+    hm[d] = vv * (uh - harh2);
+    vw[d] = vv;
+  }
+  dp[1] = dsq(hp[0], hp[1], hp[2]);
+  dp[2] = dsq(hp[1], hp[2], hp[3]);
+  dm[2] = dsq(hm[1], hm[2], hm[3]);
+  dm[3] = dsq(hm[2], hm[3], hm[4]);
+  f2 fprev(0.0f);
+  const bool ok0 = k0 < nt, ok1 = k1 < nt;
+  T* outp = a.out + (size_t)mem * nr * nt + (size_t)j0 * nt;
+  const T* dup = du + j0;
+  const T* ftp = &ftw[0][lane];
+  const f2 idth(a.inv_dtheta), idrh(a.inv_drho);
+  const T* vc0 = v + kv0;
+  const T* vc1 = v + kv1;
+  const int vwrap = (halo ? nr + 6 : nr) * nt;
+  int ov = vrow(j0 + 2) * nt, ju = wrap_idx(cj0 + j0 + 2, ng);
+  f2 vnext(vc0[ov], vc1[ov]);
+  T unext = uperp_g[ju];
+#pragma unroll 4
+  for (int r = 0; r <= rows; ++r) {
+    const f2 vv = vnext;
+    const T uu = unext;
+    if (r < rows) {
+      ov += nt;
+      ov = ov == vwrap ? 0 : ov;
+      ju = ju + 1 == ng ? 0 : ju + 1;
+      vnext = f2(vc0[ov], vc1[ov]);
+      unext = uperp_g[ju];
+    }
+    hp[5] = vv * f2(fma(half, uu, harh));
+    hm[5] = vv * f2(fma(half, uu, -harh));
+    vw[5] = vv;
+    dp[3] = dsq(hp[2], hp[3], hp[4]);
+    dm[4] = dsq(hm[3], hm[4], hm[5]);
+    const f2 f = face_pair2_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
+                              hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
+    if (r > 0) {
+      const f2 dth = (f2(ftp[1], ftp[33]) - f2(ftp[0], ftp[32])) * idth;
+      const f2 drh = (f - fprev) * idrh;
+      const f2 o = (f2(*dup) * vw[2] - dth) - drh;
+      if (ok0) outp[k0] = o.v.x;
+      if (ok1) outp[k1] = o.v.y;
+      outp += nt;
+      ++dup;
+      ftp += WT2 + 1;
+    }
+    fprev = f;
+#pragma unroll
+    for (int d = 0; d < 5; ++d) {
+      hp[d] = hp[d + 1];
+      hm[d] = hm[d + 1];
+      vw[d] = vw[d + 1];
+      dp[d] = dp[d + 1];
+      dm[d] = dm[d + 1];
+    }
+  }
+}
+
 template <typename T>
 __global__ void k_alpha_theta(const Geom g, const T* v, const T* upar, T bcoef, u64* bits, int stride) {
   const int mem = blockIdx.y;
@@ -299,8 +497,26 @@ __global__ void k_alpha_rho(const T* uperp, int nr, double* out) {
   }
 }
 
+static bool packed_f32_weno() {
+  static int on = -1;  // NWB_WENO_F32X2=0 selects the scalar fp32 kernel (measurement knob)
+  if (on < 0) {
+    const char* e = std::getenv("NWB_WENO_F32X2");
+    on = e ? (e[0] != '0') : 1;
+  }
+  return on == 1;
+}
+
 template <typename T> void launch_weno(const WenoArgs<T>& a, cudaStream_t s) {
-  dim3 grid((a.g.nt + WT - 1) / WT, (a.g.nr + WT * WWARPS - 1) / (WT * WWARPS), a.g.batch);
+  const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
+  const int gy = (nrows + WT * WWARPS - 1) / (WT * WWARPS);
+  if constexpr (sizeof(T) == 4) {
+    if (packed_f32_weno()) {
+      dim3 grid((a.g.nt + WT2 - 1) / WT2, gy, a.g.batch);
+      k_weno_f32x2<<<grid, WWARPS * 32, 0, s>>>(a);
+      return;
+    }
+  }
+  dim3 grid((a.g.nt + WT - 1) / WT, gy, a.g.batch);
   k_weno<T><<<grid, WWARPS * 32, 0, s>>>(a);
 }
 
