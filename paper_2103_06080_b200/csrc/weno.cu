@@ -281,30 +281,36 @@ __device__ __forceinline__ f2 operator-(f2 a, f2 b) {
 __device__ __forceinline__ f2 fma(f2 a, f2 b, f2 c) { return f2(__ffma2_rn(a.v, b.v, c.v)); }
 using ::fma;  // keep the scalar overloads visible next to the packed one
 
-__device__ __forceinline__ f2 face_pair2(f2 p0, f2 p1, f2 p2, f2 p3, f2 p4, f2 m0, f2 m1, f2 m2,
-                                         f2 m3, f2 m4) {
-  f2 np, dp, nm, dm;
-  face_nd(p0, p1, p2, p3, p4, dsq(p0, p1, p2), dsq(p1, p2, p3), dsq(p2, p3, p4), np, dp);
-  face_nd(m0, m1, m2, m3, m4, dsq(m0, m1, m2), dsq(m1, m2, m3), dsq(m2, m3, m4), nm, dm);
+template <typename P> struct pair_of;
+template <> struct pair_of<float> { using type = f2; };
+
+// W(p) + W(m) for both lanes of a pair, from numerators / denominators
+__device__ __forceinline__ f2 pair_div(f2 np, f2 dp, f2 nm, f2 dm) {
   const f2 d6p = f2(6.0f) * dp, d6m = f2(6.0f) * dm;
   return f2(__fdividef(np.v.x, d6p.v.x) + __fdividef(nm.v.x, d6m.v.x),
             __fdividef(np.v.y, d6p.v.y) + __fdividef(nm.v.y, d6m.v.y));
 }
-__device__ __forceinline__ f2 face_pair2_d(f2 p0, f2 p1, f2 p2, f2 p3, f2 p4, f2 Dp0, f2 Dp1,
-                                           f2 Dp2, f2 m0, f2 m1, f2 m2, f2 m3, f2 m4, f2 Dm0,
-                                           f2 Dm1, f2 Dm2) {
-  f2 np, dp, nm, dm;
+template <typename P>
+__device__ __forceinline__ P face_pair2(P p0, P p1, P p2, P p3, P p4, P m0, P m1, P m2, P m3, P m4) {
+  P np, dp, nm, dm;
+  face_nd(p0, p1, p2, p3, p4, dsq(p0, p1, p2), dsq(p1, p2, p3), dsq(p2, p3, p4), np, dp);
+  face_nd(m0, m1, m2, m3, m4, dsq(m0, m1, m2), dsq(m1, m2, m3), dsq(m2, m3, m4), nm, dm);
+  return pair_div(np, dp, nm, dm);
+}
+template <typename P>
+__device__ __forceinline__ P face_pair2_d(P p0, P p1, P p2, P p3, P p4, P Dp0, P Dp1, P Dp2, P m0,
+                                          P m1, P m2, P m3, P m4, P Dm0, P Dm1, P Dm2) {
+  P np, dp, nm, dm;
   face_nd(p0, p1, p2, p3, p4, Dp0, Dp1, Dp2, np, dp);
   face_nd(m0, m1, m2, m3, m4, Dm0, Dm1, Dm2, nm, dm);
-  const f2 d6p = f2(6.0f) * dp, d6m = f2(6.0f) * dm;
-  return f2(__fdividef(np.v.x, d6p.v.x) + __fdividef(nm.v.x, d6m.v.x),
-            __fdividef(np.v.y, d6p.v.y) + __fdividef(nm.v.y, d6m.v.y));
+  return pair_div(np, dp, nm, dm);
 }
 
 constexpr int WT2 = 64;  // columns per warp tile (two per lane)
 
-__global__ void __launch_bounds__(WWARPS * 32) k_weno_f32x2(const WenoArgs<float> a) {
-  using T = float;
+template <typename T>
+__global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
+  using P = typename pair_of<T>::type;
   __shared__ T lp[WWARPS][WT2 + 8], lm[WWARPS][WT2 + 8];  // theta split fluxes of one row
   __shared__ T ft[WWARPS][WT][WT2 + 1];                   // theta faces of the tile
   const int nr = a.g.nr, nt = a.g.nt;
@@ -338,13 +344,13 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_f32x2(const WenoArgs<float
   const int rows = min(WT, jend - j0);
 
   // ---- theta faces (faces lane and lane + 32 of each row, packed)
-  f2 vl(v[(size_t)vrow(j0) * nt + kl0], v[(size_t)vrow(j0) * nt + kl1]);
+  P vl(v[(size_t)vrow(j0) * nt + kl0], v[(size_t)vrow(j0) * nt + kl1]);
   T v_hi = lane < 6 ? v[(size_t)vrow(j0) * nt + kh] : (T)0;
   T c_cur = pi * upar[j0];
-  const f2 qb2(qb);
+  const P qb2(qb);
   for (int r = 0; r < rows; ++r) {
     const T cp = hath - c_cur, cm = -hath - c_cur;
-    const f2 sp = vl * fma(qb2, vl, f2(cp)), sm = vl * fma(qb2, vl, f2(cm));
+    const P sp = vl * fma(qb2, vl, P(cp)), sm = vl * fma(qb2, vl, P(cm));
     lpw[lane] = sp.v.x;
     lpw[lane + 32] = sp.v.y;
     lmw[lane] = sm.v.x;
@@ -355,14 +361,15 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_f32x2(const WenoArgs<float
     }
     if (r + 1 < rows) {
       const T* vn = v + (size_t)(halo ? j0 + r + 4 : j0 + r + 1) * nt;
-      vl = f2(vn[kl0], vn[kl1]);
+      vl = P(vn[kl0], vn[kl1]);
       if (lane < 6) v_hi = vn[kh];
       c_cur = pi * upar[j0 + r + 1];
     }
     __syncwarp();
-    auto P = [&](int d) { return f2(lpw[lane + d], lpw[lane + 32 + d]); };
-    auto M = [&](int d) { return f2(lmw[lane + d], lmw[lane + 32 + d]); };
-    const f2 fc = face_pair2(P(0), P(1), P(2), P(3), P(4), M(5), M(4), M(3), M(2), M(1));
+    auto lp2 = [&](int d) { return P(lpw[lane + d], lpw[lane + 32 + d]); };
+    auto lm2 = [&](int d) { return P(lmw[lane + d], lmw[lane + 32 + d]); };
+    const P fc = face_pair2(lp2(0), lp2(1), lp2(2), lp2(3), lp2(4), lm2(5), lm2(4), lm2(3), lm2(2),
+                            lm2(1));
     ftw[r][lane] = fc.v.x;
     ftw[r][lane + 32] = fc.v.y;
     __syncwarp();
@@ -386,13 +393,13 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_f32x2(const WenoArgs<float
   // ---- rho sweep down columns k0 = x0 + lane and k1 = k0 + 32 (packed)
   const int k0 = x0 + lane, k1 = k0 + 32;
   const int kv0 = wrap_idx(k0, nt), kv1 = wrap_idx(k1, nt);
-  f2 hp[6], hm[6], vw[6], dp[6], dm[6];
-  const f2 harh2(harh), half2(half);
+  P hp[6], hm[6], vw[6], dp[6], dm[6];
+  const P harh2(harh), halP(half);
 #pragma unroll
   for (int d = 0; d < 5; ++d) {
     const size_t ro = (size_t)vrow(j0 - 3 + d) * nt;
-    const f2 vv(v[ro + kv0], v[ro + kv1]);
-    const f2 uh(half * uperp_g[wrap_idx(cj0 + j0 - 3 + d, ng)]);
+    const P vv(v[ro + kv0], v[ro + kv1]);
+    const P uh(half * uperp_g[wrap_idx(cj0 + j0 - 3 + d, ng)]);
     hp[d] = vv * (uh + harh2);
     hm[d] = vv * (uh - harh2);
     vw[d] = vv;
@@ -401,40 +408,40 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_f32x2(const WenoArgs<float
   dp[2] = dsq(hp[1], hp[2], hp[3]);
   dm[2] = dsq(hm[1], hm[2], hm[3]);
   dm[3] = dsq(hm[2], hm[3], hm[4]);
-  f2 fprev(0.0f);
+  P fprev((T)0);
   const bool ok0 = k0 < nt, ok1 = k1 < nt;
   T* outp = a.out + (size_t)mem * nr * nt + (size_t)j0 * nt;
   const T* dup = du + j0;
   const T* ftp = &ftw[0][lane];
-  const f2 idth(a.inv_dtheta), idrh(a.inv_drho);
+  const P idth(a.inv_dtheta), idrh(a.inv_drho);
   const T* vc0 = v + kv0;
   const T* vc1 = v + kv1;
   const int vwrap = (halo ? nr + 6 : nr) * nt;
   int ov = vrow(j0 + 2) * nt, ju = wrap_idx(cj0 + j0 + 2, ng);
-  f2 vnext(vc0[ov], vc1[ov]);
+  P vnext(vc0[ov], vc1[ov]);
   T unext = uperp_g[ju];
 #pragma unroll 4
   for (int r = 0; r <= rows; ++r) {
-    const f2 vv = vnext;
+    const P vv = vnext;
     const T uu = unext;
     if (r < rows) {
       ov += nt;
       ov = ov == vwrap ? 0 : ov;
       ju = ju + 1 == ng ? 0 : ju + 1;
-      vnext = f2(vc0[ov], vc1[ov]);
+      vnext = P(vc0[ov], vc1[ov]);
       unext = uperp_g[ju];
     }
-    hp[5] = vv * f2(fma(half, uu, harh));
-    hm[5] = vv * f2(fma(half, uu, -harh));
+    hp[5] = vv * P(fma(half, uu, harh));
+    hm[5] = vv * P(fma(half, uu, -harh));
     vw[5] = vv;
     dp[3] = dsq(hp[2], hp[3], hp[4]);
     dm[4] = dsq(hm[3], hm[4], hm[5]);
-    const f2 f = face_pair2_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
+    const P f = face_pair2_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
                               hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
     if (r > 0) {
-      const f2 dth = (f2(ftp[1], ftp[33]) - f2(ftp[0], ftp[32])) * idth;
-      const f2 drh = (f - fprev) * idrh;
-      const f2 o = (f2(*dup) * vw[2] - dth) - drh;
+      const P dth = (P(ftp[1], ftp[33]) - P(ftp[0], ftp[32])) * idth;
+      const P drh = (f - fprev) * idrh;
+      const P o = (P(*dup) * vw[2] - dth) - drh;
       if (ok0) outp[k0] = o.v.x;
       if (ok1) outp[k1] = o.v.y;
       outp += nt;
@@ -497,8 +504,12 @@ __global__ void k_alpha_rho(const T* uperp, int nr, double* out) {
   }
 }
 
-static bool packed_f32_weno() {
-  static int on = -1;  // NWB_WENO_F32X2=0 selects the scalar fp32 kernel (measurement knob)
+// fp32 runs the two-columns-per-lane packed kernel (NWB_WENO_F32X2=0 selects
+// the scalar one: measurement knob).  An fp64 pair version (no packed fp64
+// pipe; 160 registers, 71 KB shared) would drop occupancy below the scalar
+// kernel's, which already keeps the FP64 pipe 73 % busy.
+static bool weno_x2() {
+  static int on = -1;
   if (on < 0) {
     const char* e = std::getenv("NWB_WENO_F32X2");
     on = e ? (e[0] != '0') : 1;
@@ -510,9 +521,9 @@ template <typename T> void launch_weno(const WenoArgs<T>& a, cudaStream_t s) {
   const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
   const int gy = (nrows + WT * WWARPS - 1) / (WT * WWARPS);
   if constexpr (sizeof(T) == 4) {
-    if (packed_f32_weno()) {
+    if (weno_x2()) {
       dim3 grid((a.g.nt + WT2 - 1) / WT2, gy, a.g.batch);
-      k_weno_f32x2<<<grid, WWARPS * 32, 0, s>>>(a);
+      k_weno_x2<T><<<grid, WWARPS * 32, 0, s>>>(a);
       return;
     }
   }
