@@ -1311,8 +1311,12 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     const int r = std::atoi(env);
     if ((r == 1 || r == 2 || r == 4 || r == 8) && (size_t)r * row_bytes <= 200 * 1024) p->theta_rows_c2r = r;
   }
-  int th = ((n_rho / 4) + 31) / 32 * 32;
-  p->rho_threads = th < 64 ? 64 : (th > 512 ? 512 : th);
+  // about one radix-10 butterfly per thread and pass: short columns get small
+  // CTAs, so several share an SM (C4's 1250-point columns: 128 threads, 4 CTAs
+  // per SM, rho pass 2.97 -> 1.45 ms per 256-member stage) while the 10000-point
+  // C2 column keeps 512 threads (measured best against 256 / 384 / 640 / 768)
+  int th = ((n_rho / 10) + 31) / 32 * 32;
+  p->rho_threads = th < 128 ? 128 : (th > 512 ? 512 : th);  // small grids: latency-bound, keep 4 warps
   if (p->rho_split) p->rho_threads = p->rho_threads > 256 ? 256 : p->rho_threads;
   if (const char* env = std::getenv("NWB_RHO_THREADS")) {
     const int t = std::atoi(env);

@@ -108,8 +108,11 @@ __device__ __forceinline__ int wrap_idx(int x, int n) {
 constexpr int WT = 32;      // tile edge (cells) per warp
 constexpr int WWARPS = 4;   // warps per CTA, stacked along rho
 
+#ifndef NWB_WENO_MINB
+#define NWB_WENO_MINB 1
+#endif
 template <typename T>
-__global__ void __launch_bounds__(WWARPS * 32) k_weno(const WenoArgs<T> a) {
+__global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoArgs<T> a) {
   __shared__ T lp[WWARPS][WT + 8], lm[WWARPS][WT + 8];   // theta split fluxes of one row
   __shared__ T ft[WWARPS][WT][WT + 1];                   // theta faces of the tile
   const int nr = a.g.nr, nt = a.g.nt;
