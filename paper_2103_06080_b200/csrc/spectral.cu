@@ -685,12 +685,19 @@ static inline int grid_cap(long n, int threads) {
   return (int)(b < 148L * 16 ? (b < 1 ? 1 : b) : 148L * 16);
 }
 
+// threads of a theta CTA: short rows (R m <= 2048 points, e.g. Set 1's m = 224
+// at R = 8) need about one 16-point butterfly per thread, and a 128-thread CTA
+// lets four CTAs share an SM (the kernels are bounded by 256 threads)
+template <int R> static int theta_block(int m) {
+  return R > 1 && R * m <= 2048 ? 128 : theta_threads<R>();
+}
+
 template <typename T, int R>
 static void c2r_r(const ThetaArgs<T>& a, cudaStream_t s) {
   const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_theta_c2r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
-  k_theta_c2r<T, R><<<grid, theta_threads<R>(), sm, s>>>(a);
+  k_theta_c2r<T, R><<<grid, theta_block<R>(a.g.m), sm, s>>>(a);
 }
 template <typename T, int R>
 static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
@@ -698,7 +705,7 @@ static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
   cudaFuncSetAttribute(k_theta_r2c<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
   dim3 grid((nrows + R - 1) / R, a.g.batch);
-  k_theta_r2c<T, R><<<grid, theta_threads<R>(), sm, s>>>(a);
+  k_theta_r2c<T, R><<<grid, theta_block<R>(a.g.m), sm, s>>>(a);
 }
 
 static int sm_count() {
