@@ -16,6 +16,7 @@
 // per thread); the rho pass prefetches its combine operands into L2 with
 // bulk (TMA) prefetches at entry so they arrive while the forward FFT runs.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -689,6 +690,12 @@ static inline int grid_cap(long n, int threads) {
 // at R = 8) need about one 16-point butterfly per thread, and a 128-thread CTA
 // lets four CTAs share an SM (the kernels are bounded by 256 threads)
 template <int R> static int theta_block(int m) {
+  static int knob = -1;  // NWB_THETA_THREADS=<64..256> measurement override
+  if (knob < 0) {
+    const char* e = std::getenv("NWB_THETA_THREADS");
+    knob = e ? std::atoi(e) : 0;
+  }
+  if (knob >= 64 && knob <= theta_threads<R>() && knob % 32 == 0) return knob;
   return R > 1 && R * m <= 2048 ? 128 : theta_threads<R>();
 }
 

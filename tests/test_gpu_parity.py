@@ -39,6 +39,21 @@ def test_weno_vs_golden(cuda, golden, name):
     assert rel_l2(golden[f"weno_{name}_out32"], got32) <= 1e-6
 
 
+@pytest.mark.parametrize("shape", [(1250, 448), (257, 130), (3, 5), (16, 2048), (130, 70),
+                                   (33, 96)])
+def test_weno_fp32_packed_vs_oracle(cuda, oracle, shape):
+    """fp32 WENO runs k_weno_x2 (two columns per lane on the packed FFMA2 pipe):
+    partial 64-column tiles, periodic wrap, extents below one tile."""
+    rng = np.random.default_rng(7 + sum(shape))
+    v = rng.standard_normal(shape).astype(np.float32)
+    up, uq, du = (np.float32(0.03) * rng.standard_normal(shape[0]).astype(np.float32)
+                  for _ in range(3))
+    ref = oracle.weno5_b(v, up, uq, du, 0.05, 0.32, 0.21)
+    got = nw.weno5_b(v, up, uq, du, np.float32(0.05), 0.32, 0.21)
+    assert got.dtype == np.float32 and got.shape == shape
+    assert rel_l2(ref, got) <= 1e-6
+
+
 @pytest.mark.parametrize("shape", [(1250, 448), (257, 130), (3, 5), (16, 2048)])
 def test_weno_vs_oracle_random_shapes(cuda, oracle, shape):
     rng = np.random.default_rng(sum(shape))
