@@ -1293,9 +1293,12 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     return fail(NWB_EUNSUPPORTED, "transform length exceeds one CTA's shared memory");
   }
   const size_t row_bytes = (size_t)p->g.m * csz;
+  // rows per theta CTA: the largest R with R rows in <= 64 KB of shared memory that
+  // still gives >= 2 CTAs per SM over the whole batch (small single grids such as
+  // C1 / C3 otherwise leave SMs idle)
   p->theta_rows = 1;
   for (int r : {8, 4, 2})
-    if ((size_t)r * row_bytes <= 64 * 1024) {
+    if ((size_t)r * row_bytes <= 64 * 1024 && (long)batch * ((n_rho + r - 1) / r) >= 2L * 148) {
       p->theta_rows = r;
       break;
     }

@@ -54,8 +54,11 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 // threads per theta CTA: 128 per staged row up to 256 (one-row CTAs are
 // small, so more of them -- in different phases -- share an SM)
 template <int R> constexpr int theta_threads() { return R == 1 ? 128 : 256; }
+#ifndef NWB_THETA_MINB_R1
+#define NWB_THETA_MINB_R1 4
+#endif
 template <typename T, int R> constexpr int theta_min_blocks() {
-  return R == 1 ? (sizeof(T) == 8 ? 4 : 6) : (sizeof(T) == 8 ? NWB_THETA_MINB64 : 3);
+  return R == 1 ? (sizeof(T) == 8 ? NWB_THETA_MINB_R1 : 6) : (sizeof(T) == 8 ? NWB_THETA_MINB64 : 3);
 }
 // an fp32 rho column (<= 113 KB) leaves room for a second CTA per SM, whose
 // loads then overlap this one's transforms

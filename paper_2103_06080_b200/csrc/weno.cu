@@ -111,16 +111,18 @@ constexpr int WWARPS = 4;   // warps per CTA, stacked along rho
 #ifndef NWB_WENO_MINB
 #define NWB_WENO_MINB 1
 #endif
-template <typename T>
+// WTR: rows per warp tile (32; 16 / 8 for small grids, where more, shorter warps
+// finish sooner -- the extra rho halo and faces are cheap there)
+template <typename T, int WTR>
 __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoArgs<T> a) {
   __shared__ T lp[WWARPS][WT + 8], lm[WWARPS][WT + 8];   // theta split fluxes of one row
-  __shared__ T ft[WWARPS][WT][WT + 1];                   // theta faces of the tile
+  __shared__ T ft[WWARPS][WTR][WT + 1];                  // theta faces of the tile
   const int nr = a.g.nr, nt = a.g.nt;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mem = blockIdx.z;
   const int x0 = blockIdx.x * WT;
   const int jend = a.row_end ? a.row_end : nr;
-  const int j0 = a.row_begin + (blockIdx.y * WWARPS + w) * WT;
+  const int j0 = a.row_begin + (blockIdx.y * WWARPS + w) * WTR;
   if (j0 >= jend) return;  // warp-uniform
   const int row = (a.step_ctr ? *a.step_ctr : 0) + a.row_off;
   // coefficient rows are global (rho slab: local row j is global cj0 + j)
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
   T(*ftw)[WT + 1] = ft[w];
   const int kl = wrap_idx(x0 + lane - 3, nt);     // column loaded by this lane (line slot lane)
   const int kh = wrap_idx(x0 + lane + 29, nt);    // extra slot 32 + lane for lanes < 6
-  const int rows = min(WT, jend - j0);
+  const int rows = min(WTR, jend - j0);
 
   // ---- theta faces, row by row: face f of a row lies between tile columns f-1 and f
   // software-pipelined: row r+1 is loaded while row r's faces are computed
@@ -311,17 +313,17 @@ __device__ __forceinline__ P face_pair2_d(P p0, P p1, P p2, P p3, P p4, P Dp0, P
 
 constexpr int WT2 = 64;  // columns per warp tile (two per lane)
 
-template <typename T>
+template <typename T, int WTR>
 __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   using P = typename pair_of<T>::type;
   __shared__ T lp[WWARPS][WT2 + 8], lm[WWARPS][WT2 + 8];  // theta split fluxes of one row
-  __shared__ T ft[WWARPS][WT][WT2 + 1];                   // theta faces of the tile
+  __shared__ T ft[WWARPS][WTR][WT2 + 1];                   // theta faces of the tile
   const int nr = a.g.nr, nt = a.g.nt;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mem = blockIdx.z;
   const int x0 = blockIdx.x * WT2;
   const int jend = a.row_end ? a.row_end : nr;
-  const int j0 = a.row_begin + (blockIdx.y * WWARPS + w) * WT;
+  const int j0 = a.row_begin + (blockIdx.y * WWARPS + w) * WTR;
   if (j0 >= jend) return;  // warp-uniform
   const int row = (a.step_ctr ? *a.step_ctr : 0) + a.row_off;
   const int cld = a.coef_ld ? a.coef_ld : nr, cj0 = a.coef_j0, ng = a.nr_glob ? a.nr_glob : nr;
@@ -344,7 +346,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   // lanes < 6 also slot 64 + lane
   const int kl0 = wrap_idx(x0 + lane - 3, nt), kl1 = wrap_idx(x0 + lane + 29, nt);
   const int kh = wrap_idx(x0 + lane + 61, nt);
-  const int rows = min(WT, jend - j0);
+  const int rows = min(WTR, jend - j0);
 
   // ---- theta faces (faces lane and lane + 32 of each row, packed)
   P vl(v[(size_t)vrow(j0) * nt + kl0], v[(size_t)vrow(j0) * nt + kl1]);
@@ -520,18 +522,27 @@ static bool weno_x2() {
   return on == 1;
 }
 
-template <typename T> void launch_weno(const WenoArgs<T>& a, cudaStream_t s) {
+template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, cudaStream_t s) {
   const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
-  const int gy = (nrows + WT * WWARPS - 1) / (WT * WWARPS);
+  const int gy = (nrows + WTR * WWARPS - 1) / (WTR * WWARPS);
   if constexpr (sizeof(T) == 4) {
     if (weno_x2()) {
       dim3 grid((a.g.nt + WT2 - 1) / WT2, gy, a.g.batch);
-      k_weno_x2<T><<<grid, WWARPS * 32, 0, s>>>(a);
+      k_weno_x2<T, WTR><<<grid, WWARPS * 32, 0, s>>>(a);
       return;
     }
   }
   dim3 grid((a.g.nt + WT - 1) / WT, gy, a.g.batch);
-  k_weno<T><<<grid, WWARPS * 32, 0, s>>>(a);
+  k_weno<T, WTR><<<grid, WWARPS * 32, 0, s>>>(a);
+}
+
+// rows per warp tile: 32 unless the grid has fewer than ~2048 tiles (small
+// single grids), then 16 or 8 so more warps run shorter sweeps
+template <typename T> void launch_weno(const WenoArgs<T>& a, cudaStream_t s) {
+  const long tiles = (long)((a.g.nt + WT - 1) / WT) * ((a.g.nr + WT - 1) / WT) * a.g.batch;
+  if (a.row_end || tiles >= 2048) launch_weno_t<T, 32>(a, s);
+  else if (tiles >= 1024) launch_weno_t<T, 16>(a, s);
+  else launch_weno_t<T, 8>(a, s);
 }
 
 template <typename T>
