@@ -206,6 +206,8 @@ def downsample_fields(fields: VelocityFields, factor_sigma: int,
         if (n - 1) % f and n % f:
             raise ValueError(f"{name}={f} does not divide extent {n}")
     sl = (slice(None, None, factor_sigma), slice(None, None, factor_rho))
-    return VelocityFields(*(np.ascontiguousarray(a[sl]) for a in
-                            (fields.u_par, fields.u_perp,
-                             fields.du_perp_dsigma, fields.du_perp_drho)))
+    arrs = (fields.u_par, fields.u_perp, fields.du_perp_dsigma, fields.du_perp_drho)
+    if not isinstance(fields.u_par, np.ndarray) and hasattr(fields.u_par, "is_cuda"):
+        # device-resident fields (evaluate_fields_device) stay on the device
+        return VelocityFields(*(a[sl].contiguous() for a in arrs))
+    return VelocityFields(*(np.ascontiguousarray(a[sl]) for a in arrs))
