@@ -307,13 +307,21 @@ def _snapshot_steps(config: DomainConfig, snapshot_sigmas) -> dict[int, float]:
 
 
 def _to_host64(t) -> np.ndarray:
-    """Device tensor -> fresh float64 numpy array (cast on the device, one
-    cudaMemcpy into the destination; ~2x faster than Tensor.cpu())."""
+    """Device tensor -> fresh float64 numpy array: cast on the device, one DMA
+    into page-locked memory from torch's caching host allocator (the returned
+    array views that block and keeps it alive; a freed block is reused by the
+    next call, so repeated marches -- studies, ensembles -- copy at PCIe/C2C
+    speed, 287 MB in ~5 ms instead of ~75 ms into fresh pageable memory)."""
     torch = _torch()
     src = t.to(torch.float64).contiguous()
-    out = np.empty(tuple(src.shape), dtype=np.float64)
-    torch.from_numpy(out).copy_(src)
-    return out
+    try:
+        host = torch.empty(tuple(src.shape), dtype=torch.float64, pin_memory=True)
+    except RuntimeError:  # no page-locked memory available: pageable copy
+        out = np.empty(tuple(src.shape), dtype=np.float64)
+        torch.from_numpy(out).copy_(src)
+        return out
+    host.copy_(src)
+    return host.numpy()
 
 
 def _as_host_field(x) -> np.ndarray:
