@@ -267,7 +267,8 @@ struct nwb_plan {
   int theta_rows_c2r = 1;    // c2r (transposed reads) favours many small CTAs for long rows
   int theta_stream_rows = 0;  // R of the streaming theta kernels (0 = not used)
   int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
-  int rho_prefetch = 0;      // bulk L2 prefetch of combine operands (NWB_RHO_PREFETCH overrides)
+  int rho_prefetch = 0;      // bulk L2 prefetch of combine operands, percent of each row (NWB_RHO_PREFETCH)
+  int rho_next_pf = 0;       // L2 prefetch of column k + rho_next_pf's input (NWB_RHO_NEXTPF)
   int rho_debug = 0;
   int theta_debug = 0;       // NWB_THETA_DEBUG (never set in production)         // NWB_RHO_DEBUG measurement knobs (never set in production)
   int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
@@ -368,6 +369,7 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.zero_stride = 4;
   a.split = p->rho_split;
   a.prefetch = p->rho_prefetch;
+  a.next_pf = p->rho_next_pf;
   a.debug = p->rho_debug;
   a.persistent = p->rho_persistent;
   a.dh2 = p->dh2;
@@ -1110,7 +1112,7 @@ template <typename T> int slab_rho_impl(nwb_slab* s, int mode, const void* bt, v
   q.P12 = (const cplx<T>*)s->P12;
   q.P2 = (const cplx<T>*)s->P2;
   q.ds = (T)s->d_sigma;
-  q.prefetch = 1;
+  q.prefetch = 100;
   launch_rho<T>(q, mode, s->rho_threads, s->stream);
   CHECK_LAUNCH("slab rho");
   return NWB_OK;
@@ -1273,7 +1275,11 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     // bulk L2 prefetch of the combine operands: off (measured slower at Set 4
     // in both precisions since the radix-R passes and two fp32 CTAs per SM)
     p->rho_prefetch = 0;
-    if (const char* env = std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = env[0] == '1';
+    if (const char* env = std::getenv("NWB_RHO_PREFETCH")) {  // "1" = whole rows, else percent
+      const int v = std::atoi(env);
+      p->rho_prefetch = v == 1 ? 100 : (v < 0 ? 0 : (v > 100 ? 100 : v));
+    }
+    if (const char* env = std::getenv("NWB_RHO_NEXTPF")) p->rho_next_pf = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_DEBUG")) p->rho_debug = std::atoi(env);
     if (const char* env = std::getenv("NWB_THETA_DEBUG")) p->theta_debug = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_PERSIST")) p->rho_persistent = env[0] == '1';
@@ -1326,6 +1332,19 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     if (t >= 32 && t <= (p->rho_split ? 256 : 1024) && t % 32 == 0) p->rho_threads = t;
   }
   cudaError_t e = cudaSetDevice(device);
+  // Long single-grid columns (C2: 10000 points, one fp64 / two fp32 CTAs per SM):
+  // bulk-prefetch the head of the combine operand rows into L2 at CTA entry and,
+  // after the combine, the input column of the CTA one resident wave later (the
+  // next CTA on this SM), so part of the streaming overlaps the transforms.
+  // Measured at C2 (tools/rho_probe.py, profiles/README.md): fp64 rho
+  // 1.146 -> 1.104 ms per step with 40 % / one wave, fp32 0.590 -> 0.581 with 25 %.
+  if (e == cudaSuccess && batch == 1 && (size_t)n_rho * csz >= 64 * 1024 && !p->rho_split) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    const int per_sm = (int)(smem_max / ((size_t)n_rho * csz * 9 / 8));
+    if (!std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = p->rsz == 8 ? 40 : 25;
+    if (!std::getenv("NWB_RHO_NEXTPF")) p->rho_next_pf = sms * (per_sm < 1 ? 1 : per_sm);
+  }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete p;

@@ -77,7 +77,8 @@ template <typename T> struct RhoArgs {
   const cplx<T>* tw_h2;
   const cplx<T>* tw_split;
   int split;
-  int prefetch;               // bulk L2 prefetch of the combine operands at entry
+  int prefetch;               // bulk L2 prefetch of the combine operands at entry: percent of each row
+  int next_pf;                // > 0: prefetch the input column k + next_pf into L2 after the combine
   int debug;                  // measurement knobs (NWB_RHO_DEBUG): 1 skip FFTs, 2 skip combine loads
   int persistent;             // march modes run k_rho_stream (one CTA per SM walking columns)
 };

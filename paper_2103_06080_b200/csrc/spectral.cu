@@ -417,19 +417,21 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   }
   if (a.prefetch && threadIdx.x == 0) {
     // the combine operands are consumed after the forward FFT: start their
-    // DRAM -> L2 traffic now so it overlaps the transform
+    // DRAM -> L2 traffic now so it overlaps the transform (the first
+    // a.prefetch percent of each row: the combine walks the rows head first)
+    const int np = a.prefetch >= 100 ? n : (int)((long)n * a.prefetch / 100);
     if (MODE == RHO_STAGE1) {
-      prefetch_row(a.vh + row, n);
-      prefetch_row(a.E + trow, n);
-      prefetch_row(a.P1 + trow, n);
-      prefetch_row(a.P12 + trow, n);
+      prefetch_row(a.vh + row, np);
+      prefetch_row(a.E + trow, np);
+      prefetch_row(a.P1 + trow, np);
+      prefetch_row(a.P12 + trow, np);
     } else if (MODE == RHO_STAGE2) {
-      prefetch_row(a.u + row, n);
-      prefetch_row(a.P2 + trow, n);
+      prefetch_row(a.u + row, np);
+      prefetch_row(a.P2 + trow, np);
     } else if (MODE == RHO_EULER) {
-      prefetch_row(a.vh + row, n);
-      prefetch_row(a.E + trow, n);
-      prefetch_row(a.P1 + trow, n);
+      prefetch_row(a.vh + row, np);
+      prefetch_row(a.E + trow, np);
+      prefetch_row(a.P1 + trow, np);
     }
   }
   if (MODE == RHO_INV_NAT) {
@@ -456,6 +458,8 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   if (!(a.debug & 4))
     rho_combine<T, MODE>(x, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
                          a.vh + row, a.u + row, a.ds, a.debug);
+  if (a.next_pf && threadIdx.x == 0 && k + a.next_pf < a.g.kk)
+    prefetch_row(a.in + row + (size_t)a.next_pf * a.g.ld, n);  // a later CTA's column input
   __syncthreads();
   if (!(a.debug & 1)) fft_inverse(x, a.dr, 1, 0, a.tw_r);
   V* dst = a.out + row;
