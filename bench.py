@@ -185,13 +185,51 @@ KERNELS = ("theta_c2r", "weno", "theta_r2c", "rho_stage1", "theta_c2r", "weno", 
            "rho_stage2")
 
 
+def table_read_fraction(n: int) -> float:
+    """Share of each multiplier-table row the rho combine reads: tables are
+    read at the canonical +-f position (csrc/fft.cuh sym_pos), i.e. block 0 of
+    the first-stage radix r1 plus half of the other blocks.  r1 restates the
+    host planner (capi.cu plan_fft, max product 16, no split)."""
+    m, c = n, {}
+    for r in (2, 3, 5, 7):
+        c[r] = 0
+        while m % r == 0:
+            m //= r
+            c[r] += 1
+    c2 = c[2]
+    c2 -= min(c[7], c2)                       # 7 pairs with 2
+    for _ in range(c[5]):                      # 5 pairs with 3, else 2
+        if c[3] > 0:
+            c[3] -= 1
+        elif c2 > 0:
+            c2 -= 1
+    c3 = c[3]
+    while c3 > 0:                              # 3.4 / 3.3 / 3.2 / 3
+        if c2 >= 2:
+            c2 -= 2; c3 -= 1
+        elif c3 >= 2:
+            c3 -= 2
+        elif c2 >= 1:
+            c2 -= 1; c3 -= 1
+        else:
+            c3 -= 1
+    head = {1: 2, 2: 4, 3: 8}.get(c2 % 4)
+    r1 = head or (7 if c[7] else 5 if c[5] else 3 if c[3] else 4 if n % 4 == 0 else n)
+    if r1 <= 1 or n % r1:
+        return 1.0
+    mm = n // r1
+    canon = mm + ((r1 - 1) // 2) * mm + ((mm + 1) // 2 if r1 % 2 == 0 else 0)
+    return canon / n
+
+
 def algorithmic_bytes(cfg, precision: str, batch: int = 1):
     """Compulsory HBM bytes per launch of each kernel slot.
 
     Per member: theta c2r / r2c and WENO move 1 field in + 1 out; the rho
     passes stream b~ and the state (Vh, U) plus write two spectra; the
     multiplier tables (E, Phi1, Phi1m2 in stage 1, Phi2 in stage 2) are read
-    once per launch and shared by all members of a batch.
+    once per launch, shared by all members of a batch, and only at canonical
+    +-f positions (table_read_fraction of each row).
     """
     r = 8 if precision == "double" else 4
     phys = cfg.N_rho * cfg.N_theta * r
@@ -199,8 +237,9 @@ def algorithmic_bytes(cfg, precision: str, batch: int = 1):
     c2r = batch * (spec + phys)
     weno = batch * 2 * phys
     r2c = batch * (phys + spec)
-    rho1 = batch * 4 * spec + 3 * spec   # read b~, Vh; write U, T*; tables E, Phi1, Phi1m2
-    rho2 = batch * 4 * spec + 1 * spec   # read b~, U; write Vh, T; table Phi2
+    tf = table_read_fraction(cfg.N_rho)  # 0.6 at N_rho = 10000 (r1 = 5)
+    rho1 = batch * 4 * spec + int(3 * spec * tf)  # read b~, Vh; write U, T*; E, Phi1, Phi1m2
+    rho2 = batch * 4 * spec + int(spec * tf)      # read b~, U; write Vh, T; Phi2
     return [c2r, weno, r2c, rho1, c2r, weno, r2c, rho2]
 
 

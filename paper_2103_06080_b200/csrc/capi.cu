@@ -205,6 +205,10 @@ void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& t
   if (const char* env = std::getenv(n == pad_env_n() ? "NWB_PAD" : "NWB_PAD_OTHER")) d.pad_period = std::atoi(env);
   if ((size_t)padded_len(n, d.pad_period) * sizeof(cplx<T>) > 227u * 1024u) d.pad_period = 0;
   d.pad_magic = d.pad_period ? magic_for(d.pad_period) : 0u;
+  d.sym_r1 = h.stages.empty() ? 0 : h.stages[0];
+  if (const char* env = std::getenv("NWB_RHO_SYM")) if (env[0] == '0') d.sym_r1 = 0;  // measurement knob
+  d.sym_m = d.sym_r1 > 0 ? n / d.sym_r1 : n;
+  d.sym_magic = d.sym_r1 > 0 && d.sym_m > 1 ? magic_for(d.sym_m) : 0u;
   st = 0;
   for (int p = 0; p < d.np; ++p) {
     const int ra = h.passes[p].first, rb = h.passes[p].second;
@@ -569,6 +573,7 @@ template <typename T> int create_impl(nwb_plan* p) {
     half.passes.assign(p->plan_r.passes.begin() + 1, p->plan_r.passes.end());
     std::vector<cplx<T>> tw2;
     build_desc<T>(g.nr / 2, half, p->dh2, tw2);
+    p->dh2.sym_r1 = 0;  // the split kernel reads its own half of each table row
     auto tws = twiddles<T>(g.nr, g.nr / 2);
     TRY(dalloc(p, &p->tw_h2, tw2.size() * C));
     TRY(dalloc(p, &p->tw_split, tws.size() * C));

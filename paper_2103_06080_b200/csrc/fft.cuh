@@ -44,6 +44,11 @@ struct FftDesc {
   int pfast[NWB_MAX_PASSES];          // pad_period divides s_b: strides pre-padded
   int psa_p[NWB_MAX_PASSES];          // padded s_a, s_b (valid when pfast)
   int psb_p[NWB_MAX_PASSES];
+  // j <-> -j symmetry of the digit-reversed output (first-stage radix r1,
+  // block length M = n / r1; sym_r1 = 0: off): see sym_pos
+  int sym_r1;
+  int sym_m;
+  unsigned sym_magic;                 // magic for x / M
 };
 
 // physical slot of logical element e in a (padded) shared-memory line
@@ -53,6 +58,24 @@ __device__ __forceinline__ int pidx(const FftDesc& d, int e) {
 // padded line length for n logical elements
 __host__ __device__ inline int padded_len(int n, int pad_period) {
   return pad_period ? n + n / pad_period + 1 : n + 1;  // one slot of slack (c2r stages X[n])
+}
+
+// Canonical position of p under f -> -f (mod n).  With p = q1 M + rest
+// (q1 the first-stage digit, i.e. f = q1 (mod r1)), negating f gives
+// digits r1 - q1, r_i - 1 - q_i (q1 != 0), so the partner position is
+// (r1 - q1) M + (M - 1 - rest): blocks 1 .. r1-1 pair up in reverse order
+// and block 0 (f = 0 mod r1) is kept whole.  Tables that depend on f only
+// through xi_f^2 (the phi multipliers, bitwise symmetric) are read at the
+// canonical position, so 55-60 % of each table row is ever touched and the
+// mirrored half comes from L2 (same column, read earlier in the walk).
+__device__ __forceinline__ int sym_pos(const FftDesc& d, int p) {
+  if (d.sym_r1 <= 1) return p;
+  const int q1 = d.sym_magic ? (int)__umulhi((unsigned)p, d.sym_magic) : p;
+  if (q1 == 0) return p;
+  const int rest = p - q1 * d.sym_m;
+  const int q2 = d.sym_r1 - q1;
+  if (q1 < q2 || (q1 == q2 && 2 * rest <= d.sym_m - 1)) return p;
+  return q2 * d.sym_m + (d.sym_m - 1 - rest);
 }
 
 // ------------------------------------------------------------ butterflies

@@ -366,12 +366,13 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
       if (p < n) {
         sp[q] = pidx(d, p);
         b[q] = x[sp[q]];
+        const int tp = sym_pos(d, p);  // tables: canonical +-f position
         if (MODE == RHO_STAGE1 && !nl) {
-          o1[q] = E[p]; o2[q] = vh[p]; o3[q] = P1[p]; o4[q] = P12[p];
+          o1[q] = E[tp]; o2[q] = vh[p]; o3[q] = P1[tp]; o4[q] = P12[tp];
         } else if (MODE == RHO_STAGE2) {
-          o1[q] = P2[p]; o2[q] = u[p];
+          o1[q] = P2[tp]; o2[q] = u[p];
         } else if (MODE == RHO_EULER) {
-          o1[q] = E[p]; o2[q] = vh[p]; o3[q] = P1[p];
+          o1[q] = E[tp]; o2[q] = vh[p]; o3[q] = P1[tp];
         }
       }
     }

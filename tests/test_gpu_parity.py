@@ -378,3 +378,30 @@ def test_c3_with_device_medium(cuda, golden, golden_meta):
     rep = nw.run_exprk22(c3, nw.initial_nwave(rho, theta, c3.A, c3.B), f)
     assert max_relative(golden["c3_double_final_sub"], rep.final.values[::8]) <= FP64_FIELD
     assert abs(rep.max_abs_v - golden_meta["runs"]["c3_double"]["max_abs_v"]) <= 1e-12
+
+
+@pytest.mark.parametrize("n_rho,n_theta,precision,scheme", [
+    (64, 56, "double", "exprk22"), (45, 56, "double", "exprk22"), (105, 70, "double", "expeuler"),
+    (98, 48, "single", "exprk22"), (10000, 64, "double", "exprk22")])
+def test_symmetric_table_reads_bitwise(cuda, monkeypatch, n_rho, n_theta, precision, scheme):
+    """The rho combine reads the phi tables at the canonical +-f position
+    (fft.cuh sym_pos); the tables are bitwise j <-> -j symmetric, so the march
+    must be bitwise identical to full-row reads (NWB_RHO_SYM=0)."""
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    cfg = nw.DomainConfig(N_rho=n_rho, N_theta=n_theta, N_sigma=4, Sigma=1.6)
+    _, rho, theta = nw.build_axes(cfg)
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B)).values
+    eps = nw.EPS_DOUBLE if precision == "double" else nw.EPS_SINGLE
+    outs = []
+    for sym in ("0", "1"):
+        monkeypatch.setenv("NWB_RHO_SYM", sym)
+        plan = DevicePlan(n_rho, n_theta, 1, precision, cfg.d_sigma, cfg.rho_span,
+                          cfg.theta_span, cfg.A, cfg.B, eps)
+        plan.set_coeffs(None, None, None, n_rows=8)
+        plan.load_physical(v0)
+        plan.march(scheme, 0, 4)
+        out, _ = plan.store_physical()
+        outs.append(out.cpu().numpy())
+        plan.close()
+    assert np.array_equal(outs[0], outs[1])

@@ -172,7 +172,9 @@ def test_bench_roofline_bookkeeping():
     b = bench.algorithmic_bytes(cfg, "double")
     F = cfg.N_rho * cfg.N_theta * 8
     spec = cfg.N_rho * (cfg.N_theta // 2 + 1) * 16
-    assert b[1] == 2 * F and b[3] == 7 * spec and b[7] == 5 * spec
+    # tables read at canonical +-f positions: 60 % of each row at N_rho = 10000 (r1 = 5)
+    assert bench.table_read_fraction(cfg.N_rho) == pytest.approx(0.6)
+    assert b[1] == 2 * F and b[3] == 4 * spec + int(1.8 * spec) and b[7] == 4 * spec + int(0.6 * spec)
     blk = bench.roofline_block(cfg, "c2", "double", [1.0, 2.0, 1.0, 3.0, 1.0, 2.0, 1.0, 2.5], 1)
     # both rho stages are one kernel (k_rho): 5.5 ms beats WENO's 4 ms
     assert blk["kernel"] == "rho_pass" and blk["unit"] == "GB/s"
@@ -182,4 +184,54 @@ def test_bench_roofline_bookkeeping():
     assert blk["kernel"] == "weno"
     # tables are shared by the members of a batch
     b4 = bench.algorithmic_bytes(cfg, "double", 4)
-    assert b4[3] == 4 * 4 * spec + 3 * spec and b4[1] == 4 * 2 * F
+    assert b4[3] == 4 * 4 * spec + int(1.8 * spec) and b4[1] == 4 * 2 * F
+
+
+def _freq_of_pos(n, stages):
+    f = []
+    for p in range(n):
+        rem, ff, mult, L = p, 0, 1, n
+        for r in stages:
+            s = L // r
+            q = rem // s
+            rem -= q * s
+            ff += q * mult
+            mult *= r
+            L = s
+        f.append(ff)
+    return f
+
+
+def _sym_pos(p, r1, m):
+    """Python restatement of csrc/fft.cuh sym_pos."""
+    q1 = p // m
+    if q1 == 0:
+        return p
+    rest = p - q1 * m
+    q2 = r1 - q1
+    if q1 < q2 or (q1 == q2 and 2 * rest <= m - 1):
+        return p
+    return q2 * m + (m - 1 - rest)
+
+
+@pytest.mark.parametrize("stages", [[5, 2, 5, 2, 5, 2, 5, 2], [2, 5, 5, 2, 2, 2, 5, 5], [4, 4, 2],
+                                    [3, 3, 5], [7, 2, 7], [8, 5, 5, 2], [5], [2, 2], [3, 5, 7]])
+def test_symmetric_table_position_map(stages):
+    """sym_pos maps every digit-reversed position to one holding the same |f|
+    (f or n - f), is idempotent, folds every block but the first onto its
+    mirror, and touches about half of each table row."""
+    n = int(np.prod(stages))
+    freq = _freq_of_pos(n, stages)
+    pos_of = {f: p for p, f in enumerate(freq)}
+    m = n // stages[0]
+    canon = set()
+    for p in range(n):
+        c = _sym_pos(p, stages[0], m)
+        assert freq[c] in (freq[p], (n - freq[p]) % n)
+        assert _sym_pos(c, stages[0], m) == c
+        canon.add(c)
+        # outside block 0 (f = 0 mod r1, kept whole) the partner of p maps to
+        # the same canonical position
+        if p >= m:
+            assert _sym_pos(pos_of[(n - freq[p]) % n], stages[0], m) == c
+    assert len(canon) <= n // 2 + m + 1
