@@ -251,11 +251,11 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback"
 
 
-def ncu_traffic(config: str, precision: str, kernel: str):
+def ncu_traffic(config: str, precision: str, kernel: str, key: str = "dram_bytes_per_launch"):
     try:
         with open(TRAFFIC_FILE) as fh:
             t = json.load(fh)
-        return t[config][precision][kernel]["dram_bytes_per_launch"]
+        return t[config][precision][kernel][key]
     except Exception:
         return None
 
@@ -281,11 +281,20 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
     dom = max(by_kernel, key=lambda k: by_kernel[k]["ms"])
     d = by_kernel[dom]
     achieved = d["bytes"] / d["n"] / (d["ms"] / d["n"] * 1e-3) / 1e9
-    return {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-            "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "traffic": ncu_traffic(cname, precision, dom),
-            "share_of_step": round(d["ms"] / step_ms, 4),
-            "per_kernel": per}
+    blk = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+           "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+           "traffic": ncu_traffic(cname, precision, dom),
+           "share_of_step": round(d["ms"] / step_ms, 4),
+           "per_kernel": per}
+    if dom == "weno":
+        # WENO moves 2F per launch but is arithmetic-bound (no tensor-core form):
+        # its limiter is the FP64 pipe (fp64) / the FMA-pipe issue rate (fp32),
+        # from the committed ncu capture (profiles/ncu_traffic.json)
+        key = "fp64_pipe_pct" if precision == "double" else "fma_pipe_pct"
+        blk["limiter"] = {"pipe": "fp64" if precision == "double" else "fma",
+                          "busy_pct_ncu": ncu_traffic(cname, precision, dom, key),
+                          "issue_pct_ncu": ncu_traffic(cname, precision, dom, "issue_pct")}
+    return blk
 
 
 # ------------------------------------------------------------------ arms

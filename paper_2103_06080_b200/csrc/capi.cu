@@ -209,6 +209,7 @@ void build_desc(int n, const FftPlanHost& h, FftDesc& d, std::vector<cplx<T>>& t
   if (const char* env = std::getenv("NWB_RHO_SYM")) if (env[0] == '0') d.sym_r1 = 0;  // measurement knob
   d.sym_m = d.sym_r1 > 0 ? n / d.sym_r1 : n;
   d.sym_magic = d.sym_r1 > 0 && d.sym_m > 1 ? magic_for(d.sym_m) : 0u;
+  d.sym_n = d.sym_r1 > 1 ? d.sym_m + (d.sym_r1 - 1) / 2 * d.sym_m + (d.sym_r1 % 2 == 0 ? (d.sym_m + 1) / 2 : 0) : n;
   st = 0;
   for (int p = 0; p < d.np; ++p) {
     const int ra = h.passes[p].first, rb = h.passes[p].second;
@@ -273,9 +274,12 @@ struct nwb_plan {
   int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
   int rho_prefetch = 0;      // bulk L2 prefetch of combine operands, percent of each row (NWB_RHO_PREFETCH)
   int rho_next_pf = 0;       // L2 prefetch of column k + rho_next_pf's input (NWB_RHO_NEXTPF)
+  int rho_roll = 0;          // combine: L2 prefetch of the operands rho_roll rounds ahead (NWB_RHO_ROLL)
   int rho_debug = 0;
   int theta_debug = 0;       // NWB_THETA_DEBUG (never set in production)         // NWB_RHO_DEBUG measurement knobs (never set in production)
   int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
+  int rho_ws = 0, rho_ws2 = 0, rho_ws_ctas = 0;  // warp-specialised rho pass (k_rho_ws) group sizes, CTAs
+  void* ws_scratch = nullptr;
   FftDesc dh2{};             // half-column descriptor (split mode)
   void *tw_h2 = nullptr, *tw_split = nullptr;
   size_t rsz = 8;  // sizeof(real)
@@ -376,6 +380,12 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.next_pf = p->rho_next_pf;
   a.debug = p->rho_debug;
   a.persistent = p->rho_persistent;
+  a.ws_threads = p->rho_ws;
+  a.ws_threads2 = p->rho_ws2;
+  a.ws_ctas = p->rho_ws_ctas;
+  a.roll = p->rho_roll;
+  if (const char* env = std::getenv("NWB_RHO_WS_DEBUG")) a.ws_debug = std::atoi(env);
+  a.scratch = (cplx<T>*)p->ws_scratch;
   a.dh2 = p->dh2;
   a.tw_h2 = (const cplx<T>*)p->tw_h2;
   a.tw_split = (const cplx<T>*)p->tw_split;
@@ -526,6 +536,7 @@ template <typename T> int create_impl(nwb_plan* p) {
   TRY(dalloc(p, &p->P2, tab));
   TRY(dalloc(p, (void**)&p->red, (size_t)g.batch * 4 * sizeof(u64)));
   TRY(dalloc(p, (void**)&p->step_ctr, sizeof(int)));
+  if (p->rho_ws > 0) TRY(dalloc(p, &p->ws_scratch, (size_t)p->rho_ws_ctas * 2 * g.ld * C));
   CU(cudaMemsetAsync(p->red, 0, (size_t)g.batch * 4 * sizeof(u64), p->stream));
   CU(cudaMemsetAsync(p->step_ctr, 0, sizeof(int), p->stream));
   // zero the padding columns once so nothing uninitialised is ever read
@@ -1285,10 +1296,20 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
       p->rho_prefetch = v == 1 ? 100 : (v < 0 ? 0 : (v > 100 ? 100 : v));
     }
     if (const char* env = std::getenv("NWB_RHO_NEXTPF")) p->rho_next_pf = std::atoi(env);
+    if (const char* env = std::getenv("NWB_RHO_ROLL")) p->rho_roll = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_DEBUG")) p->rho_debug = std::atoi(env);
     if (const char* env = std::getenv("NWB_THETA_DEBUG")) p->theta_debug = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_PERSIST")) p->rho_persistent = env[0] == '1';
     if (p->rho_debug) p->rho_persistent = 0;  // the knobs live in k_rho
+    // warp-specialised rho pass: NWB_RHO_WS=<transform threads>[,<combine threads>]
+    if (const char* env = std::getenv("NWB_RHO_WS")) {
+      int a1 = 0, a2 = 256;
+      if (std::sscanf(env, "%d,%d", &a1, &a2) >= 1 && a1 >= 64 && a1 % 32 == 0 && a2 >= 32 &&
+          a2 % 32 == 0 && a1 + a2 <= 512 && !p->rho_debug) {
+        p->rho_ws = a1;
+        p->rho_ws2 = a2;
+      }
+    }
   }
   int mp_r = 16, mp_h = 16;
   if (const char* env = std::getenv("NWB_MAXPROD_R")) mp_r = std::atoi(env);
@@ -1349,6 +1370,15 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     const int per_sm = (int)(smem_max / ((size_t)n_rho * csz * 9 / 8));
     if (!std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = p->rsz == 8 ? 40 : 25;
     if (!std::getenv("NWB_RHO_NEXTPF")) p->rho_next_pf = sms * (per_sm < 1 ? 1 : per_sm);
+    // and the combine prefetches each round's operand rows one round ahead
+    // (fp64 rho 1.060 -> 1.034 ms per step, fp32 0.601 -> 0.582)
+    if (!std::getenv("NWB_RHO_ROLL")) p->rho_roll = 1;
+  }
+  if (e == cudaSuccess && p->rho_ws > 0) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    p->rho_ws_ctas = sms > 0 ? sms : 148;
+    p->rho_split = 0;
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {

@@ -49,6 +49,7 @@ struct FftDesc {
   int sym_r1;
   int sym_m;
   unsigned sym_magic;                 // magic for x / M
+  int sym_n;                          // canonical positions form the prefix [0, sym_n)
 };
 
 // physical slot of logical element e in a (padded) shared-memory line
@@ -250,7 +251,7 @@ __device__ __forceinline__ unsigned fdiv(unsigned x, unsigned magic) {
 // conjugate roots and twiddles (unnormalised inverse transform).
 template <int RA, int RB, bool DIT, bool CONJ, typename V>
 __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows, int rstride,
-                                         const V* __restrict__ tw) {
+                                         const V* __restrict__ tw, int tid, int nth) {
   const int L = d.pspan[p];
   const int sa = L / RA;            // stage-a span
   const int sb = sa / RB;           // lane range
@@ -258,7 +259,7 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
   const int total = per_row * rows;
   const V* twa = tw + d.pofs_a[p];
   const V* fia = tw + d.pfin_a[p];
-  for (int g = threadIdx.x; g < total; g += blockDim.x) {
+  for (int g = tid; g < total; g += nth) {
     const int row = (int)fdiv((unsigned)g, d.pmag_row[p]);
     const int h = g - row * per_row;
     const int blk = (int)fdiv((unsigned)h, d.pmag_sb[p]);
@@ -359,21 +360,21 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
 // pass type codes (host planner in capi.cu): 10*ra + rb
 template <bool DIT, bool CONJ, typename V>
 __device__ __forceinline__ void run_pass(V* x, const FftDesc& d, int p, int rows, int rstride,
-                                         const V* tw) {
+                                         const V* tw, int tid = threadIdx.x, int nth = blockDim.x) {
   switch (d.ptype[p]) {
-    case 21: fft_pass<2, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 31: fft_pass<3, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 41: fft_pass<4, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 51: fft_pass<5, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 71: fft_pass<7, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 81: fft_pass<8, 1, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 72: fft_pass<7, 2, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 53: fft_pass<5, 3, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 52: fft_pass<5, 2, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 34: fft_pass<3, 4, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 33: fft_pass<3, 3, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    case 32: fft_pass<3, 2, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
-    default: fft_pass<4, 4, DIT, CONJ>(x, d, p, rows, rstride, tw); break;
+    case 21: fft_pass<2, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 31: fft_pass<3, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 41: fft_pass<4, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 51: fft_pass<5, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 71: fft_pass<7, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 81: fft_pass<8, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 72: fft_pass<7, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 53: fft_pass<5, 3, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 52: fft_pass<5, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 34: fft_pass<3, 4, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 33: fft_pass<3, 3, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 32: fft_pass<3, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    default: fft_pass<4, 4, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
   }
 }
 
@@ -398,6 +399,27 @@ __device__ void fft_inverse(V* x, const FftDesc& d, int rows, int rstride, const
   for (int p = d.np - 1; p >= first_pass; --p) {
     run_pass<true, true>(x, d, p, rows, rstride, tw);
     __syncthreads();
+  }
+}
+
+// Group variants for warp-specialised kernels: threads [tid0, tid0 + nth) of
+// the CTA run the transform and synchronise on named barrier BAR only (the
+// other warps of the CTA never touch it).
+template <int BAR> __device__ __forceinline__ void group_sync(int nth) {
+  asm volatile("bar.sync %0, %1;" ::"n"(BAR), "r"(nth) : "memory");
+}
+template <int BAR, typename V>
+__device__ void fft_forward_grp(V* x, const FftDesc& d, const V* tw, int tid, int nth) {
+  for (int p = 0; p < d.np; ++p) {
+    run_pass<false, false>(x, d, p, 1, 0, tw, tid, nth);
+    group_sync<BAR>(nth);
+  }
+}
+template <int BAR, typename V>
+__device__ void fft_inverse_grp(V* x, const FftDesc& d, const V* tw, int tid, int nth) {
+  for (int p = d.np - 1; p >= 0; --p) {
+    run_pass<true, true>(x, d, p, 1, 0, tw, tid, nth);
+    group_sync<BAR>(nth);
   }
 }
 

@@ -79,8 +79,16 @@ template <typename T> struct RhoArgs {
   int split;
   int prefetch;               // bulk L2 prefetch of the combine operands at entry: percent of each row
   int next_pf;                // > 0: prefetch the input column k + next_pf into L2 after the combine
+  int roll;                   // > 0: the combine prefetches its operands roll rounds ahead into L2
   int debug;                  // measurement knobs (NWB_RHO_DEBUG): 1 skip FFTs, 2 skip combine loads
   int persistent;             // march modes run k_rho_stream (one CTA per SM walking columns)
+  // warp-specialised pass (k_rho_ws): transform / combine group sizes (0 = off),
+  // CTAs (<= SMs x CTAs per SM) and their scratch (2 rows of ld per CTA)
+  int ws_threads;
+  int ws_threads2;
+  int ws_ctas;
+  int ws_debug;               // measurement: 1 = combine group idle, 2 = transform group skips FFTs
+  cplx<T>* scratch;
 };
 
 template <typename T> struct WenoArgs {

@@ -346,25 +346,44 @@ template <typename V> __device__ __forceinline__ void prefetch_row(const V* p, i
 // any result is stored (the row pointers are __restrict__), so each thread
 // keeps 4U independent 16-byte loads in flight -- the combine is a pure
 // stream and needs that memory-level parallelism.
-template <typename T, int MODE>
+// XG: x is a global scratch row in plain position order (the warp-specialised
+// pass, k_rho_ws) instead of the padded shared-memory line.
+template <typename T, int MODE, bool XG = false>
 __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
                                             const cplx<T>* __restrict__ E,
                                             const cplx<T>* __restrict__ P1,
                                             const cplx<T>* __restrict__ P12,
                                             const cplx<T>* __restrict__ P2,
                                             cplx<T>* __restrict__ vh, cplx<T>* __restrict__ u,
-                                            T ds, int debug) {
+                                            T ds, int debug, int tid = threadIdx.x,
+                                            int nth = blockDim.x, int roll = 0) {
   using V = cplx<T>;
   constexpr int U = 4;
   const bool nl = debug & 2;
-  for (int p0 = threadIdx.x; p0 < n; p0 += U * blockDim.x) {
+  for (int p0 = tid; p0 < n; p0 += U * nth) {
+    if (roll > 0 && tid == 0) {
+      // rolling L2 prefetch of the rows this CTA reads `roll` rounds from now
+      // (tables only inside their canonical prefix [0, sym_n))
+      const int s0 = p0 + roll * U * nth, s1 = min(s0 + U * nth, n), t1 = min(s1, d.sym_n);
+      if (s0 < s1) {
+        const unsigned nb = (unsigned)((s1 - s0) * sizeof(V)) & ~15u;
+        if (MODE == RHO_STAGE1 || MODE == RHO_EULER) prefetch_l2_bulk(vh + s0, nb);
+        if (MODE == RHO_STAGE2) prefetch_l2_bulk(u + s0, nb);
+      }
+      if (s0 < t1) {
+        const unsigned nb = (unsigned)((t1 - s0) * sizeof(V)) & ~15u;
+        if (MODE == RHO_STAGE1 || MODE == RHO_EULER) { prefetch_l2_bulk(E + s0, nb); prefetch_l2_bulk(P1 + s0, nb); }
+        if (MODE == RHO_STAGE1) prefetch_l2_bulk(P12 + s0, nb);
+        if (MODE == RHO_STAGE2) prefetch_l2_bulk(P2 + s0, nb);
+      }
+    }
     V b[U], o1[U], o2[U], o3[U], o4[U];
     int sp[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      const int p = p0 + q * blockDim.x;
+      const int p = p0 + q * nth;
       if (p < n) {
-        sp[q] = pidx(d, p);
+        sp[q] = XG ? p : pidx(d, p);
         b[q] = x[sp[q]];
         const int tp = sym_pos(d, p);  // tables: canonical +-f position
         if (MODE == RHO_STAGE1 && !nl) {
@@ -378,7 +397,7 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      const int p = p0 + q * blockDim.x;
+      const int p = p0 + q * nth;
       if (p >= n) continue;
       const V bb = b[q];
       if (MODE == RHO_STAGE1) {
@@ -458,7 +477,7 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   // debug bit 4 (measurement only): transforms without any global traffic
   if (!(a.debug & 4))
     rho_combine<T, MODE>(x, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
-                         a.vh + row, a.u + row, a.ds, a.debug);
+                         a.vh + row, a.u + row, a.ds, a.debug, threadIdx.x, blockDim.x, a.roll);
   if (a.next_pf && threadIdx.x == 0 && k + a.next_pf < a.g.kk)
     prefetch_row(a.in + row + (size_t)a.next_pf * a.g.ld, n);  // a later CTA's column input
   __syncthreads();
@@ -467,6 +486,75 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   if (!(a.debug & 4))
     for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+}
+
+// ------------------------------------------------------------------ rho pass, warp-specialised
+// One 160 KB fp64 column fills an SM's shared memory, so in k_rho the SM
+// alternates between transforming and streaming.  Here a persistent CTA splits
+// into two warp groups that run concurrently on different columns:
+//   G1 (threads [0, nfft)): transforms.  Iteration i: inverse of column i-2
+//      (combined row read back from an L2-resident scratch slot) and store of
+//      its result, then load + forward transform of column i, written to the
+//      scratch slot i & 1.  Its barriers are named barrier 1 over G1 only.
+//   G2 (the remaining warps): the stage combine of column i-1 on its scratch
+//      slot -- all the table / state / U streaming -- while G1 transforms.
+// One __syncthreads per iteration hands the slots over (it orders the
+// global-memory scratch traffic within the CTA).  The scratch (2 slots per
+// CTA, 47 MB at C2 fp64) stays in L2; HBM sees the same compulsory bytes as
+// k_rho.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(512, 1) k_rho_ws(const RhoArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* x = reinterpret_cast<V*>(smem_raw);
+  const int n = a.dr.n;
+  const int items = a.g.batch * a.g.kk;
+  const int nfft = a.ws_threads;
+  const bool fft_group = (int)threadIdx.x < nfft;
+  const int tid2 = (int)threadIdx.x - nfft, nth2 = (int)blockDim.x - nfft;
+  V* const scr = a.scratch + (size_t)blockIdx.x * 2 * a.g.ld;
+  const int ncol = (int)blockIdx.x < items ? (items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  for (int i = 0; i < ncol + 2; ++i) {
+    if (fft_group) {
+      const int tid = threadIdx.x;
+      if (i >= 2) {
+        const int w = blockIdx.x + (i - 2) * gridDim.x;
+        const int mem = w % a.g.batch, k = w / a.g.batch;
+        const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+        const V* sc = scr + (size_t)(i & 1) * a.g.ld;
+        for (int j = tid; j < n; j += nfft) cp_async_c(&x[pidx(a.dr, j)], &sc[j]);
+        cp_async_wait_all();
+        group_sync<1>(nfft);
+        if (!(a.ws_debug & 2)) fft_inverse_grp<1>(x, a.dr, a.tw_r, tid, nfft);
+        V* dst = a.out + row;
+        for (int j = tid; j < n; j += nfft) dst[j] = x[pidx(a.dr, j)];
+        if (a.step_ctr && mem == 0 && k == 0 && tid == 0) *a.step_ctr += 1;
+        group_sync<1>(nfft);  // the line is refilled below
+      }
+      if (i < ncol) {
+        const int w = blockIdx.x + i * gridDim.x;
+        const int mem = w % a.g.batch, k = w / a.g.batch;
+        const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+        const V* src = a.in + row;
+        for (int j = tid; j < n; j += nfft) cp_async_c(&x[pidx(a.dr, j)], &src[j]);
+        cp_async_wait_all();
+        if (a.zero_bits && k == 0 && tid == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
+        group_sync<1>(nfft);
+        if (!(a.ws_debug & 2)) fft_forward_grp<1>(x, a.dr, a.tw_r, tid, nfft);
+        V* sc = scr + (size_t)(i & 1) * a.g.ld;
+        for (int j = tid; j < n; j += nfft) sc[j] = x[pidx(a.dr, j)];
+      }
+    } else if (i >= 1 && i - 1 < ncol && !(a.ws_debug & 1)) {
+      const int w = blockIdx.x + (i - 1) * gridDim.x;
+      const int mem = w % a.g.batch, k = w / a.g.batch;
+      const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+      const size_t trow = (size_t)k * a.g.ld;
+      V* sc = scr + (size_t)((i - 1) & 1) * a.g.ld;
+      rho_combine<T, MODE, true>(sc, a.dr, n, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
+                                 a.vh + row, a.u + row, a.ds, 0, tid2, nth2);
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ rho pass, persistent
@@ -779,6 +867,16 @@ static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
       dim3 grid(2 * a.g.batch, a.g.kk);
       k_rho_split<T, MODE><<<grid, threads, sm, s>>>(a);
       return;
+    }
+    if constexpr (MODE != RHO_INIT) {
+      if (a.ws_threads > 0 && a.scratch) {
+        const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);
+        cudaFuncSetAttribute(k_rho_ws<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const long items = (long)a.g.batch * a.g.kk;
+        const long ctas = std::min<long>(items, (long)a.ws_ctas);
+        k_rho_ws<T, MODE><<<(int)ctas, a.ws_threads + a.ws_threads2, sm, s>>>(a);
+        return;
+      }
     }
     if (a.persistent) {
       const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);

@@ -405,3 +405,37 @@ def test_symmetric_table_reads_bitwise(cuda, monkeypatch, n_rho, n_theta, precis
         outs.append(out.cpu().numpy())
         plan.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("knobs", [{"NWB_RHO_WS": "256"}, {"NWB_RHO_ROLL": "2"},
+                                   {"NWB_RHO_PREFETCH": "100", "NWB_RHO_NEXTPF": "148"}])
+@pytest.mark.parametrize("n_rho,n_theta,batch,precision", [
+    (625, 448, 1, "double"), (10000, 64, 1, "double"), (50, 56, 3, "double"),
+    (1000, 448, 1, "single")])
+def test_rho_pass_variants_bitwise(cuda, monkeypatch, knobs, n_rho, n_theta, batch, precision):
+    """Scheduling variants of the rho pass (warp-specialised k_rho_ws, rolling
+    and entry L2 prefetches) only move data earlier or elsewhere: the march is
+    bitwise identical to the default pass."""
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    cfg = nw.DomainConfig(N_rho=n_rho, N_theta=n_theta, N_sigma=4, Sigma=1.6)
+    _, rho, theta = nw.build_axes(cfg)
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B)).values
+    if batch > 1:
+        v0 = np.stack([v0 * (1.0 + 0.1 * i) for i in range(batch)])
+    eps = nw.EPS_DOUBLE if precision == "double" else nw.EPS_SINGLE
+    outs = []
+    for env in ({}, knobs):
+        for k in ("NWB_RHO_WS", "NWB_RHO_ROLL", "NWB_RHO_PREFETCH", "NWB_RHO_NEXTPF"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = DevicePlan(n_rho, n_theta, batch, precision, cfg.d_sigma, cfg.rho_span,
+                          cfg.theta_span, cfg.A, cfg.B, eps)
+        plan.set_coeffs(None, None, None, n_rows=8)
+        plan.load_physical(v0)
+        plan.march("exprk22", 0, 4)
+        out, _ = plan.store_physical()
+        outs.append(out.cpu().numpy())
+        plan.close()
+    assert np.array_equal(outs[0], outs[1])

@@ -28,6 +28,10 @@ def main(rep, config, precision):
     hdr, units, data = rows[0], rows[1], rows[2:]
     ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
     it = hdr.index("gpu__time_duration.sum")
+    pipes = {k: hdr.index(m) for k, m in (
+        ("fp64_pipe_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+        ("fma_pipe_pct", "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+        ("issue_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed")) if m in hdr}
     acc = {}
     for d in data:
         name = d[hdr.index("Kernel Name")].split("<")[0].replace("void ", "").split("::")[-1]
@@ -35,7 +39,9 @@ def main(rep, config, precision):
         if not g:
             continue
         b = scale(d[ir], units[ir]) + scale(d[iw], units[iw])
-        e = acc.setdefault(g, {"bytes": 0.0, "n": 0, "us": 0.0})
+        e = acc.setdefault(g, {"bytes": 0.0, "n": 0, "us": 0.0, **{k: 0.0 for k in pipes}})
+        for k, i in pipes.items():
+            e[k] += float(d[i])
         e["bytes"] += b
         e["n"] += 1
         e["us"] += float(d[it]) * (1e-3 if units[it] == "ns" else 1.0)
@@ -44,7 +50,8 @@ def main(rep, config, precision):
     table = json.load(open(path)) if os.path.exists(path) else {}
     table.setdefault(config, {})[precision] = {
         g: {"dram_bytes_per_launch": round(e["bytes"] / e["n"]), "launches": e["n"],
-            "ncu_us_per_launch": round(e["us"] / e["n"], 1), "report": os.path.basename(rep)}
+            "ncu_us_per_launch": round(e["us"] / e["n"], 1), "report": os.path.basename(rep),
+            **{k: round(e[k] / e["n"], 1) for k in pipes}}
         for g, e in acc.items()}
     with open(path, "w") as fh:
         json.dump(table, fh, indent=1, sort_keys=True)
