@@ -13,7 +13,7 @@ import os
 import subprocess
 import sys
 
-GROUPS = {"k_theta_c2r": "theta_c2r", "k_theta_r2c": "theta_r2c", "k_weno": "weno",
+GROUPS = {"k_theta_c2r": "theta_c2r", "k_theta_r2c": "theta_r2c", "k_weno": "weno", "k_weno_x2": "weno",
           "k_rho": "rho_pass"}
 
 
