@@ -294,6 +294,16 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
         blk["limiter"] = {"pipe": "fp64" if precision == "double" else "fma",
                           "busy_pct_ncu": ncu_traffic(cname, precision, dom, key),
                           "issue_pct_ncu": ncu_traffic(cname, precision, dom, "issue_pct")}
+        # and the largest bandwidth-bound kernel's HBM figures beside it
+        hb = max((g for g in by_kernel if g != "weno"), key=lambda g: by_kernel[g]["ms"],
+                 default=None)
+        if hb is not None:
+            e = by_kernel[hb]
+            ach = e["bytes"] / e["n"] / (e["ms"] / e["n"] * 1e-3) / 1e9
+            blk["hbm_kernel"] = {"kernel": hb, "achieved": round(ach, 1),
+                                 "frac": round(ach / peak, 4),
+                                 "traffic": ncu_traffic(cname, precision, hb),
+                                 "share_of_step": round(e["ms"] / step_ms, 4)}
     return blk
 
 
