@@ -98,6 +98,11 @@ __device__ __forceinline__ T face_pair(T p0, T p1, T p2, T p3, T p4, T m0, T m1,
                      m2, m3, m4, dsq(m0, m1, m2), dsq(m1, m2, m3), dsq(m2, m3, m4));
 }
 
+// products that must round on their own (never contracted into a following
+// add), like the split fluxes the row-by-row version stages in shared memory
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+
 __device__ __forceinline__ int wrap_idx(int x, int n) {
   if (x < 0) x += n;
   if (x >= n) x -= n;
@@ -113,10 +118,20 @@ constexpr int WWARPS = 4;   // warps per CTA, stacked along rho
 #endif
 // WTR: rows per warp tile (32; 16 / 8 for small grids, where more, shorter warps
 // finish sooner -- the extra rho halo and faces are cheap there)
-template <typename T, int WTR>
+//
+// WALK (32-row tiles): the theta faces are computed like the rho ones -- the
+// warp stages its 32 x 38 tile of V in shared memory, then lane r walks row r
+// with a 6-deep register window, so every split flux and second-difference
+// term is evaluated once per slot instead of once per stencil use (about 17
+// fewer FP64 instructions per cell, 2 shared loads per cell instead of 10).
+// The faces overwrite the row in place (face f is stored after slot f + 5 was
+// read).  Bitwise equal to the row-by-row version (same operands, same order).
+constexpr int WTS = WT + 9;  // walk tile row stride: odd (conflict-free half-warps), >= 38 slots
+template <typename T, int WTR, bool WALK>
 __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoArgs<T> a) {
-  __shared__ T lp[WWARPS][WT + 8], lm[WWARPS][WT + 8];   // theta split fluxes of one row
-  __shared__ T ft[WWARPS][WTR][WT + 1];                  // theta faces of the tile
+  constexpr int FTS = WALK ? WTS : WT + 1;                // theta-face row stride
+  __shared__ T lp[WALK ? 1 : WWARPS][WT + 8], lm[WALK ? 1 : WWARPS][WT + 8];  // split fluxes of one row
+  __shared__ T ft[WWARPS][WTR][FTS];                     // theta faces of the tile (WALK: V first)
   const int nr = a.g.nr, nt = a.g.nt;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mem = blockIdx.z;
@@ -141,18 +156,64 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
   const T hath = half * ath, harh = half * arh;
   const T* v = a.v + (size_t)mem * (halo ? nr + 6 : nr) * nt;
   auto vrow = [&](int jj) { return halo ? jj + 3 : wrap_idx(jj, nr); };
-  T* lpw = lp[w];
-  T* lmw = lm[w];
-  T(*ftw)[WT + 1] = ft[w];
+  T* lpw = lp[WALK ? 0 : w];
+  T* lmw = lm[WALK ? 0 : w];
+  T(*ftw)[FTS] = ft[w];
   const int kl = wrap_idx(x0 + lane - 3, nt);     // column loaded by this lane (line slot lane)
   const int kh = wrap_idx(x0 + lane + 29, nt);    // extra slot 32 + lane for lanes < 6
   const int rows = min(WTR, jend - j0);
 
+  if constexpr (WALK) {
+    // ---- theta faces, lane r walks row r: stage the tile's V (slot s = column x0 + s - 3)
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {
+      const T* vr = v + (size_t)vrow(j0 + r) * nt;
+      ftw[r][lane] = vr[kl];
+      if (lane < 6) ftw[r][32 + lane] = vr[kh];
+    }
+    __syncwarp();
+    if (lane < rows) {
+      const T c = mul_rn(pi, upar[j0 + lane]);
+      const T cp = hath - c, cm = -hath - c;
+      T* tr = ftw[lane];
+      // p / m: split fluxes at window slots 0..5; dp[s] = dsq(p[s-1], p[s], p[s+1]),
+      // dm[s] = dsq(m[s+1], m[s], m[s-1]) (the argument orders of face_pair)
+      T p[6], m[6], dp[6], dm[6];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        const T vv = tr[d];
+        p[d] = mul_rn(vv, fma(qb, vv, cp));
+        m[d] = mul_rn(vv, fma(qb, vv, cm));
+      }
+      dp[1] = dsq(p[0], p[1], p[2]);
+      dp[2] = dsq(p[1], p[2], p[3]);
+      dm[2] = dsq(m[3], m[2], m[1]);
+      dm[3] = dsq(m[4], m[3], m[2]);
+#pragma unroll 6
+      for (int f = 0; f <= WT; ++f) {
+        const T vv = tr[f + 5];
+        p[5] = mul_rn(vv, fma(qb, vv, cp));
+        m[5] = mul_rn(vv, fma(qb, vv, cm));
+        dp[3] = dsq(p[2], p[3], p[4]);
+        dm[4] = dsq(m[5], m[4], m[3]);
+        tr[f] = face_pair_d(p[0], p[1], p[2], p[3], p[4], dp[1], dp[2], dp[3], m[5], m[4], m[3],
+                            m[2], m[1], dm[4], dm[3], dm[2]);
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          p[d] = p[d + 1];
+          m[d] = m[d + 1];
+          dp[d] = dp[d + 1];
+          dm[d] = dm[d + 1];
+        }
+      }
+    }
+    __syncwarp();
+  } else {
   // ---- theta faces, row by row: face f of a row lies between tile columns f-1 and f
   // software-pipelined: row r+1 is loaded while row r's faces are computed
   T v_lo = v[(size_t)vrow(j0) * nt + kl];
   T v_hi = lane < 6 ? v[(size_t)vrow(j0) * nt + kh] : (T)0;
-  T c_cur = pi * upar[j0];
+  T c_cur = mul_rn(pi, upar[j0]);
   for (int r = 0; r < rows; ++r) {
     const T cp = hath - c_cur, cm = -hath - c_cur;  // c_cur = pi u_par
     lpw[lane] = v_lo * fma(qb, v_lo, cp);
@@ -165,7 +226,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
       const T* vn = v + (size_t)(halo ? j0 + r + 4 : j0 + r + 1) * nt;  // rows j0..j0+rows-1 < nr
       v_lo = vn[kl];
       if (lane < 6) v_hi = vn[kh];
-      c_cur = pi * upar[j0 + r + 1];
+      c_cur = mul_rn(pi, upar[j0 + r + 1]);
     }
     __syncwarp();
     ftw[r][lane] = face_pair(lpw[lane], lpw[lane + 1], lpw[lane + 2], lpw[lane + 3], lpw[lane + 4],
@@ -175,18 +236,20 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
   // 33rd theta face of row `lane` (between tile columns 31 and 32)
   if (lane < rows) {
     const int j = j0 + lane;
-    const T cp = hath - pi * upar[j], cm = -hath - pi * upar[j];
+    const T c = mul_rn(pi, upar[j]);
+    const T cp = hath - c, cm = -hath - c;
     const T* vr = v + (size_t)vrow(j) * nt;
     T p[6], m[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
       const T vv = vr[wrap_idx(x0 + 29 + d, nt)];
-      p[d] = vv * fma(qb, vv, cp);
-      m[d] = vv * fma(qb, vv, cm);
+      p[d] = mul_rn(vv, fma(qb, vv, cp));
+      m[d] = mul_rn(vv, fma(qb, vv, cm));
     }
     ftw[lane][WT] = face_pair(p[0], p[1], p[2], p[3], p[4], m[5], m[4], m[3], m[2], m[1]);
   }
   __syncwarp();
+  }  // !WALK
 
   // ---- rho sweep down column k with a register window of rows j-3 .. j+2
   const int k = x0 + lane;
@@ -249,7 +312,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
       }
       outp += nt;
       ++dup;
-      ftp += WT + 1;
+      ftp += FTS;
     }
     fprev = f;
 #pragma unroll
@@ -522,6 +585,14 @@ static bool weno_x2() {
   return on == 1;
 }
 
+// theta faces by row walk (NWB_WENO_WALK=0 selects the row-by-row version:
+// measurement knob); 32-row tiles only -- 16 / 8-row tiles would idle lanes
+// read per launch (the step graphs capture the choice once)
+static bool weno_walk() {
+  const char* e = std::getenv("NWB_WENO_WALK");
+  return !e || e[0] != '0';
+}
+
 template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, cudaStream_t s) {
   const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
   const int gy = (nrows + WTR * WWARPS - 1) / (WTR * WWARPS);
@@ -533,7 +604,8 @@ template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, c
     }
   }
   dim3 grid((a.g.nt + WT - 1) / WT, gy, a.g.batch);
-  k_weno<T, WTR><<<grid, WWARPS * 32, 0, s>>>(a);
+  if (WTR == 32 && weno_walk()) k_weno<T, WTR, true><<<grid, WWARPS * 32, 0, s>>>(a);
+  else k_weno<T, WTR, false><<<grid, WWARPS * 32, 0, s>>>(a);
 }
 
 // rows per warp tile: 32 unless the grid has fewer than ~2048 tiles (small

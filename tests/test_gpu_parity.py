@@ -439,3 +439,39 @@ def test_rho_pass_variants_bitwise(cuda, monkeypatch, knobs, n_rho, n_theta, bat
         outs.append(out.cpu().numpy())
         plan.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n_rho,n_theta,batch,precision", [
+    (2048, 1024, 1, "double"), (2025, 1050, 1, "double"), (1000, 448, 5, "double"),
+    (2025, 1050, 1, "single")])
+def test_weno_theta_walk_bitwise(cuda, monkeypatch, n_rho, n_theta, batch, precision):
+    """The row-walk theta faces of k_weno (32-row tiles; NWB_WENO_WALK=0 selects
+    the row-by-row version) evaluate the same operands in the same order: the
+    march, and the WENO operator alone, are bitwise identical."""
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    cfg = nw.DomainConfig(N_rho=n_rho, N_theta=n_theta, N_sigma=3, Sigma=1.2)
+    _, rho, theta = nw.build_axes(cfg)
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B)).values
+    if batch > 1:
+        v0 = np.stack([v0 * (1.0 + 0.1 * i) for i in range(batch)])
+    eps = nw.EPS_DOUBLE if precision == "double" else nw.EPS_SINGLE
+    rng = np.random.default_rng(7)
+    v = rng.standard_normal((n_rho, n_theta))
+    up, uq, du = (0.03 * rng.standard_normal(n_rho) for _ in range(3))
+    b_ops, outs = [], []
+    for walk in ("0", "1"):
+        monkeypatch.setenv("NWB_WENO_WALK", walk)
+        plan = DevicePlan(n_rho, n_theta, batch, precision, cfg.d_sigma, cfg.rho_span,
+                          cfg.theta_span, cfg.A, cfg.B, eps)
+        plan.set_coeffs(None, None, None, n_rows=8)
+        plan.load_physical(v0)
+        plan.march("exprk22", 0, 3)
+        out, _ = plan.store_physical()
+        outs.append(out.cpu().numpy())
+        plan.close()
+        if batch == 1 and precision == "double":
+            b_ops.append(np.asarray(nw.weno5_b(v, up, uq, du, 0.05, 0.32, 0.21)))
+    assert np.array_equal(outs[0], outs[1])
+    if b_ops:
+        assert np.array_equal(b_ops[0], b_ops[1])
