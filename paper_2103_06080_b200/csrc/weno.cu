@@ -376,11 +376,19 @@ __device__ __forceinline__ P face_pair2_d(P p0, P p1, P p2, P p3, P p4, P Dp0, P
 
 constexpr int WT2 = 64;  // columns per warp tile (two per lane)
 
-template <typename T, int WTR>
+// WALK (32-row tiles): lane r walks row r of the staged 32 x 70 V tile, the two
+// halves packed -- faces 0..32 from slots 0..37 (lane x) and faces 32..64 from
+// slots 32..69 (lane y) -- with the register window of k_weno's walk.  Face g
+// is stored in place at position g (g < 32, lane x) or g + 5 (lane y, right
+// after slot g + 5 is read); lane x's face 32 (its last, whose newest slot 37
+// lane y has already overwritten) is a discarded duplicate.
+constexpr int WTS2 = WT2 + 7;  // walk tile row stride: odd, >= 70 slots
+template <typename T, int WTR, bool WALK>
 __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   using P = typename pair_of<T>::type;
-  __shared__ T lp[WWARPS][WT2 + 8], lm[WWARPS][WT2 + 8];  // theta split fluxes of one row
-  __shared__ T ft[WWARPS][WTR][WT2 + 1];                   // theta faces of the tile
+  constexpr int FTS = WALK ? WTS2 : WT2 + 1;
+  __shared__ T lp[WALK ? 1 : WWARPS][WT2 + 8], lm[WALK ? 1 : WWARPS][WT2 + 8];  // split fluxes of one row
+  __shared__ T ft[WWARPS][WTR][FTS];                       // theta faces of the tile (WALK: V first)
   const int nr = a.g.nr, nt = a.g.nt;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mem = blockIdx.z;
@@ -402,19 +410,65 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   const T hath = half * ath, harh = half * arh;
   const T* v = a.v + (size_t)mem * (halo ? nr + 6 : nr) * nt;
   auto vrow = [&](int jj) { return halo ? jj + 3 : wrap_idx(jj, nr); };
-  T* lpw = lp[w];
-  T* lmw = lm[w];
-  T(*ftw)[WT2 + 1] = ft[w];
+  T* lpw = lp[WALK ? 0 : w];
+  T* lmw = lm[WALK ? 0 : w];
+  T(*ftw)[FTS] = ft[w];
   // line slot s holds column x0 + s - 3: lane loads slots lane, lane + 32, and
   // lanes < 6 also slot 64 + lane
   const int kl0 = wrap_idx(x0 + lane - 3, nt), kl1 = wrap_idx(x0 + lane + 29, nt);
   const int kh = wrap_idx(x0 + lane + 61, nt);
   const int rows = min(WTR, jend - j0);
 
+  if constexpr (WALK) {
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {
+      const T* vr = v + (size_t)vrow(j0 + r) * nt;
+      ftw[r][lane] = vr[kl0];
+      ftw[r][lane + 32] = vr[kl1];
+      if (lane < 6) ftw[r][64 + lane] = vr[kh];
+    }
+    __syncwarp();
+    if (lane < rows) {
+      const T c = mul_rn(pi, upar[j0 + lane]);
+      const P cp(hath - c), cm(-hath - c), qb2(qb);
+      T* tr = ftw[lane];
+      P p[6], m[6], dp[6], dm[6];
+#pragma unroll
+      for (int d = 0; d < 5; ++d) {
+        const P vv(tr[d], tr[32 + d]);
+        p[d] = vv * fma(qb2, vv, cp);
+        m[d] = vv * fma(qb2, vv, cm);
+      }
+      dp[1] = dsq(p[0], p[1], p[2]);
+      dp[2] = dsq(p[1], p[2], p[3]);
+      dm[2] = dsq(m[3], m[2], m[1]);
+      dm[3] = dsq(m[4], m[3], m[2]);
+#pragma unroll 6
+      for (int f = 0; f <= 32; ++f) {
+        const P vv(tr[f + 5], tr[f + 37]);
+        p[5] = vv * fma(qb2, vv, cp);
+        m[5] = vv * fma(qb2, vv, cm);
+        dp[3] = dsq(p[2], p[3], p[4]);
+        dm[4] = dsq(m[5], m[4], m[3]);
+        const P fc = face_pair2_d(p[0], p[1], p[2], p[3], p[4], dp[1], dp[2], dp[3], m[5], m[4],
+                                  m[3], m[2], m[1], dm[4], dm[3], dm[2]);
+        tr[f] = fc.v.x;
+        tr[f + 37] = fc.v.y;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+          p[d] = p[d + 1];
+          m[d] = m[d + 1];
+          dp[d] = dp[d + 1];
+          dm[d] = dm[d + 1];
+        }
+      }
+    }
+    __syncwarp();
+  } else {
   // ---- theta faces (faces lane and lane + 32 of each row, packed)
   P vl(v[(size_t)vrow(j0) * nt + kl0], v[(size_t)vrow(j0) * nt + kl1]);
   T v_hi = lane < 6 ? v[(size_t)vrow(j0) * nt + kh] : (T)0;
-  T c_cur = pi * upar[j0];
+  T c_cur = mul_rn(pi, upar[j0]);
   const P qb2(qb);
   for (int r = 0; r < rows; ++r) {
     const T cp = hath - c_cur, cm = -hath - c_cur;
@@ -431,7 +485,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
       const T* vn = v + (size_t)(halo ? j0 + r + 4 : j0 + r + 1) * nt;
       vl = P(vn[kl0], vn[kl1]);
       if (lane < 6) v_hi = vn[kh];
-      c_cur = pi * upar[j0 + r + 1];
+      c_cur = mul_rn(pi, upar[j0 + r + 1]);
     }
     __syncwarp();
     auto lp2 = [&](int d) { return P(lpw[lane + d], lpw[lane + 32 + d]); };
@@ -445,18 +499,20 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   // 65th theta face of row `lane` (between tile columns 63 and 64), scalar
   if (lane < rows) {
     const int j = j0 + lane;
-    const T cp = hath - pi * upar[j], cm = -hath - pi * upar[j];
+    const T c = mul_rn(pi, upar[j]);
+    const T cp = hath - c, cm = -hath - c;
     const T* vr = v + (size_t)vrow(j) * nt;
     T p[6], m[6];
 #pragma unroll
     for (int d = 0; d < 6; ++d) {
       const T vv = vr[wrap_idx(x0 + 61 + d, nt)];
-      p[d] = vv * fma(qb, vv, cp);
-      m[d] = vv * fma(qb, vv, cm);
+      p[d] = mul_rn(vv, fma(qb, vv, cp));
+      m[d] = mul_rn(vv, fma(qb, vv, cm));
     }
     ftw[lane][WT2] = face_pair(p[0], p[1], p[2], p[3], p[4], m[5], m[4], m[3], m[2], m[1]);
   }
   __syncwarp();
+  }  // !WALK
 
   // ---- rho sweep down columns k0 = x0 + lane and k1 = k0 + 32 (packed)
   const int k0 = x0 + lane, k1 = k0 + 32;
@@ -481,6 +537,8 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   T* outp = a.out + (size_t)mem * nr * nt + (size_t)j0 * nt;
   const T* dup = du + j0;
   const T* ftp = &ftw[0][lane];
+  // offsets of faces (lane, lane + 1, lane + 32, lane + 33) from ftp (WALK layout above)
+  const int fx1 = WALK ? (lane == 31 ? 6 : 1) : 1, fy0 = WALK ? 37 : 32, fy1 = fy0 + 1;
   const P idth(a.inv_dtheta), idrh(a.inv_drho);
   const T* vc0 = v + kv0;
   const T* vc1 = v + kv1;
@@ -507,14 +565,14 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
     const P f = face_pair2_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
                               hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
     if (r > 0) {
-      const P dth = (P(ftp[1], ftp[33]) - P(ftp[0], ftp[32])) * idth;
+      const P dth = (P(ftp[fx1], ftp[fy1]) - P(ftp[0], ftp[fy0])) * idth;
       const P drh = (f - fprev) * idrh;
       const P o = (P(*dup) * vw[2] - dth) - drh;
       if (ok0) outp[k0] = o.v.x;
       if (ok1) outp[k1] = o.v.y;
       outp += nt;
       ++dup;
-      ftp += WT2 + 1;
+      ftp += FTS;
     }
     fprev = f;
 #pragma unroll
@@ -599,7 +657,8 @@ template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, c
   if constexpr (sizeof(T) == 4) {
     if (weno_x2()) {
       dim3 grid((a.g.nt + WT2 - 1) / WT2, gy, a.g.batch);
-      k_weno_x2<T, WTR><<<grid, WWARPS * 32, 0, s>>>(a);
+      if (WTR == 32 && weno_walk()) k_weno_x2<T, WTR, true><<<grid, WWARPS * 32, 0, s>>>(a);
+      else k_weno_x2<T, WTR, false><<<grid, WWARPS * 32, 0, s>>>(a);
       return;
     }
   }

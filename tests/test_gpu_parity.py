@@ -443,11 +443,11 @@ def test_rho_pass_variants_bitwise(cuda, monkeypatch, knobs, n_rho, n_theta, bat
 
 @pytest.mark.parametrize("n_rho,n_theta,batch,precision", [
     (2048, 1024, 1, "double"), (2025, 1050, 1, "double"), (1000, 448, 5, "double"),
-    (2025, 1050, 1, "single")])
+    (2025, 1050, 1, "single"), (2048, 1024, 1, "single"), (1000, 448, 5, "single")])
 def test_weno_theta_walk_bitwise(cuda, monkeypatch, n_rho, n_theta, batch, precision):
-    """The row-walk theta faces of k_weno (32-row tiles; NWB_WENO_WALK=0 selects
-    the row-by-row version) evaluate the same operands in the same order: the
-    march, and the WENO operator alone, are bitwise identical."""
+    """The row-walk theta faces of k_weno / k_weno_x2 (32-row tiles;
+    NWB_WENO_WALK=0 selects the row-by-row version) evaluate the same operands in
+    the same order: the march, and the WENO operator alone, are bitwise identical."""
     from paper_2103_06080_b200.plan import DevicePlan
 
     cfg = nw.DomainConfig(N_rho=n_rho, N_theta=n_theta, N_sigma=3, Sigma=1.2)
@@ -470,8 +470,10 @@ def test_weno_theta_walk_bitwise(cuda, monkeypatch, n_rho, n_theta, batch, preci
         out, _ = plan.store_physical()
         outs.append(out.cpu().numpy())
         plan.close()
-        if batch == 1 and precision == "double":
-            b_ops.append(np.asarray(nw.weno5_b(v, up, uq, du, 0.05, 0.32, 0.21)))
+        if batch == 1:
+            dt = np.float64 if precision == "double" else np.float32
+            b_ops.append(np.asarray(nw.weno5_b(v.astype(dt), up.astype(dt), uq.astype(dt),
+                                               du.astype(dt), 0.05, 0.32, 0.21)))
     assert np.array_equal(outs[0], outs[1])
     if b_ops:
         assert np.array_equal(b_ops[0], b_ops[1])
