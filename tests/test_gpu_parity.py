@@ -477,3 +477,26 @@ def test_weno_theta_walk_bitwise(cuda, monkeypatch, n_rho, n_theta, batch, preci
     assert np.array_equal(outs[0], outs[1])
     if b_ops:
         assert np.array_equal(b_ops[0], b_ops[1])
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_large_host_load_staged_equals_device_load(cuda, precision):
+    """Host arrays above 64 MB go through the page-locked staging chunks of
+    plan.to_device (with the fp64 -> fp32 conversion on the host side): the
+    loaded state must equal a load of the same values from a device tensor."""
+    import torch
+
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    n_rho, n_theta = 4096, 2100  # 68.8 MB in fp64: several 32 MB chunks
+    rng = np.random.default_rng(11)
+    v0 = rng.standard_normal((n_rho, n_theta))
+    outs = []
+    for src in (v0, torch.from_numpy(v0).to("cuda:0")):
+        plan = DevicePlan(n_rho, n_theta, 1, precision, 0.01, 1.0, 1.0, 0.0, 0.0,
+                          nw.EPS_DOUBLE if precision == "double" else nw.EPS_SINGLE)
+        plan.load_physical(src)
+        out, _ = plan.store_physical()
+        outs.append(out.cpu().numpy())
+        plan.close()
+    assert np.array_equal(outs[0], outs[1])
