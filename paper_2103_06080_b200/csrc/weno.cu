@@ -27,15 +27,24 @@ namespace nwb {
 
 __device__ __forceinline__ double bits_to_real(u64 b) { return __longlong_as_double((long long)b); }
 
-// a / b to ~1 ulp: hardware reciprocal seed + two Newton steps + one
-// residual correction (no IEEE slow path; b is a positive normal here).
+// 1 / b to ~1 ulp: hardware reciprocal seed refined by one cubic step
+// (NWB_WENO_RCP3=0: two Newton steps, one more FP64 instruction); no IEEE
+// slow path -- b is a positive normal here.
+#ifndef NWB_WENO_RCP3
+#define NWB_WENO_RCP3 1
+#endif
 __device__ __forceinline__ double fast_rcp(double b) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(b));
   double e = fma(-b, r, 1.0);
+#if NWB_WENO_RCP3
+  // one cubic step r (1 + e + e^2): error ~e^3 from the seed's ~2^-22
+  return fma(r, fma(e, e, e), r);
+#else
   r = fma(r, e, r);
   e = fma(-b, r, 1.0);
   return fma(r, e, r);
+#endif
 }
 __device__ __forceinline__ float fast_rcp(float b) { return __frcp_rn(b); }
 
@@ -80,8 +89,9 @@ __device__ __forceinline__ double face_pair_d(double p0, double p1, double p2, d
   double np, dp, nm, dm;
   face_nd(p0, p1, p2, p3, p4, Dp0, Dp1, Dp2, np, dp);
   face_nd(m0, m1, m2, m3, m4, Dm0, Dm1, Dm2, nm, dm);
-  // one reciprocal for both (6 dp dm >= 6 (4e-6)^8 ~ 4e-43: normal in fp64)
-  return (np * dm + nm * dp) * fast_rcp(6.0 * (dp * dm));
+  // one reciprocal for both (dp dm >= (4e-6)^8 ~ 7e-44: normal in fp64); returns
+  // 6 F -- the 1/6 is folded into k_weno's 1/dtheta, 1/drho
+  return (np * dm + nm * dp) * fast_rcp(dp * dm);
 }
 __device__ __forceinline__ float face_pair_d(float p0, float p1, float p2, float p3, float p4,
                                              float Dp0, float Dp1, float Dp2, float m0, float m1,
@@ -275,7 +285,9 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
   T* outp = a.out + (size_t)mem * nr * nt + (size_t)j0 * nt + (col_ok ? k : 0);
   const T* dup = du + j0;
   const T* ftp = &ftw[0][lane];
-  const T idth = a.inv_dtheta, idrh = a.inv_drho;
+  // fp64 faces come as 6 F (face_pair_d)
+  const T idth = sizeof(T) == 8 ? a.inv_dtheta * (T)(1.0 / 6.0) : a.inv_dtheta;
+  const T idrh = sizeof(T) == 8 ? a.inv_drho * (T)(1.0 / 6.0) : a.inv_drho;
   // software-pipelined: the value for window slot 5 of iteration r+1 is
   // loaded while iteration r computes its face.  Running (wrapped) element
   // offset / coefficient row of the prefetched row: they advance by one row
