@@ -136,7 +136,11 @@ constexpr int WWARPS = 4;   // warps per CTA, stacked along rho
 // fewer FP64 instructions per cell, 2 shared loads per cell instead of 10).
 // The faces overwrite the row in place (face f is stored after slot f + 5 was
 // read).  Bitwise equal to the row-by-row version (same operands, same order).
-constexpr int WTS = WT + 9;  // walk tile row stride: odd (conflict-free half-warps), >= 38 slots
+constexpr int WTS = WT + 9;
+#ifndef NWB_WENO_WALK_UNROLL
+#define NWB_WENO_WALK_UNROLL 6
+#endif
+constexpr int kWalkUnroll = NWB_WENO_WALK_UNROLL;  // walk tile row stride: odd (conflict-free half-warps), >= 38 slots
 template <typename T, int WTR, bool WALK>
 __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoArgs<T> a) {
   constexpr int FTS = WALK ? WTS : WT + 1;                // theta-face row stride
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
       dp[2] = dsq(p[1], p[2], p[3]);
       dm[2] = dsq(m[3], m[2], m[1]);
       dm[3] = dsq(m[4], m[3], m[2]);
-#pragma unroll 6
+#pragma unroll kWalkUnroll
       for (int f = 0; f <= WT; ++f) {
         const T vv = tr[f + 5];
         p[5] = mul_rn(vv, fma(qb, vv, cp));
