@@ -72,7 +72,8 @@ __device__ __forceinline__ void face_nd(T a0, T a1, T a2, T a3, T a4, T D0, T D1
   const T t1 = fma(e1, e1, D1);
   const T t2 = fma(e2, e2, D2);
   const T A0 = t0 * t0, A1 = t1 * t1, A2 = t2 * t2;
-  const T q0 = fma((T)11, a2, fma((T)-7, a1, (T)2 * a0));
+  // 2 a0 - 7 a1 + 11 a2 = 2 e0 + (a1 + 5 a2): one instruction less than the direct form
+  const T q0 = fma((T)2, e0, fma((T)5, a2, a1));
   const T q1 = fma((T)2, a3, fma((T)5, a2, -a1));
   const T q2 = fma((T)5, a3, fma((T)2, a2, -a4));
   const T P = A1 * A2, x = (T)6 * A2, y = (T)3 * A1;
