@@ -74,8 +74,10 @@ __device__ __forceinline__ void face_nd(T a0, T a1, T a2, T a3, T a4, T D0, T D1
   const T A0 = t0 * t0, A1 = t1 * t1, A2 = t2 * t2;
   // 2 a0 - 7 a1 + 11 a2 = 2 e0 + (a1 + 5 a2): one instruction less than the direct form
   const T q0 = fma((T)2, e0, fma((T)5, a2, a1));
-  const T q1 = fma((T)2, a3, fma((T)5, a2, -a1));
-  const T q2 = fma((T)5, a3, fma((T)2, a2, -a4));
+  // -a1 + 5 a2 + 2 a3 = s - e1 and 2 a2 + 5 a3 - a4 = s - e2 with s = 5 a2 + a3
+  const T s5 = fma((T)5, a2, a3);
+  const T q1 = s5 - e1;
+  const T q2 = s5 - e2;
   const T P = A1 * A2, x = (T)6 * A2, y = (T)3 * A1;
   num = fma(A0, fma(x, q1, y * q2), P * q0);
   den = fma(A0, x + y, P);
