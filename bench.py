@@ -222,14 +222,18 @@ def table_read_fraction(n: int) -> float:
     return canon / n
 
 
-def algorithmic_bytes(cfg, precision: str, batch: int = 1):
-    """Compulsory HBM bytes per launch of each kernel slot.
+def algorithmic_bytes(cfg, precision: str, batch: int = 1, design: bool = False):
+    """HBM bytes per launch of each kernel slot.
 
-    Per member: theta c2r / r2c and WENO move 1 field in + 1 out; the rho
-    passes stream b~ and the state (Vh, U) plus write two spectra; the
-    multiplier tables (E, Phi1, Phi1m2 in stage 1, Phi2 in stage 2) are read
-    once per launch, shared by all members of a batch, and only at canonical
-    +-f positions (table_read_fraction of each row).
+    Algorithmic (the roofline's bytes): per member theta c2r,
+    WENO and theta r2c move one field in and one out (2F); a rho pass reads
+    two spectra (b~ and the state Vh or U) and writes two (4F).  The
+    multiplier tables are excluded (8(d)).
+
+    ``design=True`` adds what this implementation must also stream: the
+    multiplier tables (E, Phi1, Phi1m2 in stage 1, Phi2 in stage 2), read once
+    per launch for all members of a batch and only at canonical +-f positions
+    (table_read_fraction of each row).
     """
     r = 8 if precision == "double" else 4
     phys = cfg.N_rho * cfg.N_theta * r
@@ -237,9 +241,11 @@ def algorithmic_bytes(cfg, precision: str, batch: int = 1):
     c2r = batch * (spec + phys)
     weno = batch * 2 * phys
     r2c = batch * (phys + spec)
-    tf = table_read_fraction(cfg.N_rho)  # 0.6 at N_rho = 10000 (r1 = 5)
-    rho1 = batch * 4 * spec + int(3 * spec * tf)  # read b~, Vh; write U, T*; E, Phi1, Phi1m2
-    rho2 = batch * 4 * spec + int(spec * tf)      # read b~, U; write Vh, T; Phi2
+    rho1 = rho2 = batch * 4 * spec
+    if design:
+        tf = table_read_fraction(cfg.N_rho)  # 0.6 at N_rho = 10000 (r1 = 5)
+        rho1 += int(3 * spec * tf)
+        rho2 += int(spec * tf)
     return [c2r, weno, r2c, rho1, c2r, weno, r2c, rho2]
 
 
@@ -262,6 +268,7 @@ def ncu_traffic(config: str, precision: str, kernel: str, key: str = "dram_bytes
 
 def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
     abytes = algorithmic_bytes(cfg, precision, batch)
+    dbytes = algorithmic_bytes(cfg, precision, batch, design=True)
     peak, kind = hbm_peak()
     per = []
     for i, name in enumerate(KERNELS):
@@ -269,22 +276,35 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
         if ms <= 0:
             continue
         per.append({"slot": i, "kernel": name, "ms": round(ms, 5), "bytes": abytes[i],
-                    "GBs": round(abytes[i] / (ms * 1e-3) / 1e9, 1)})
+                    "GBs": round(abytes[i] / (ms * 1e-3) / 1e9, 1),
+                    "frac": round(abytes[i] / (ms * 1e-3) / 1e9 / peak, 4),
+                    "design_bytes": dbytes[i]})
     # dominant kernel type by summed time over the step
     by_kernel = {}
     for p in per:
         # both rho stages are launches of the same kernel (k_rho, two modes)
         group = "rho_pass" if p["kernel"].startswith("rho") else p["kernel"]
-        d = by_kernel.setdefault(group, {"ms": 0.0, "bytes": 0, "n": 0})
-        d["ms"] += p["ms"]; d["bytes"] += p["bytes"]; d["n"] += 1
+        d = by_kernel.setdefault(group, {"ms": 0.0, "bytes": 0, "dbytes": 0, "n": 0})
+        d["ms"] += p["ms"]; d["bytes"] += p["bytes"]; d["dbytes"] += p["design_bytes"]; d["n"] += 1
     step_ms = sum(p["ms"] for p in per)
+
+    def hbm_figures(g):
+        e = by_kernel[g]
+        sec = e["ms"] / e["n"] * 1e-3
+        ach = e["bytes"] / e["n"] / sec / 1e9
+        des = e["dbytes"] / e["n"] / sec / 1e9
+        return ach, des
+
     dom = max(by_kernel, key=lambda k: by_kernel[k]["ms"])
-    d = by_kernel[dom]
-    achieved = d["bytes"] / d["n"] / (d["ms"] / d["n"] * 1e-3) / 1e9
+    achieved, design = hbm_figures(dom)
     blk = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
            "peak_kind": kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+           "bytes_basis": "SURVEY 8(d) algorithmic: 4F per rho-pass launch, 2F per theta c2r / "
+                          "WENO / theta r2c launch, multiplier tables excluded",
+           "achieved_design": round(design, 1), "frac_design": round(design / peak, 4),
            "traffic": ncu_traffic(cname, precision, dom),
-           "share_of_step": round(d["ms"] / step_ms, 4),
+           "share_of_step": round(by_kernel[dom]["ms"] / step_ms, 4),
+           "step_frac_16F": None,
            "per_kernel": per}
     if dom == "weno":
         # WENO moves 2F per launch but is arithmetic-bound (no tensor-core form):
@@ -298,12 +318,11 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
         hb = max((g for g in by_kernel if g != "weno"), key=lambda g: by_kernel[g]["ms"],
                  default=None)
         if hb is not None:
-            e = by_kernel[hb]
-            ach = e["bytes"] / e["n"] / (e["ms"] / e["n"] * 1e-3) / 1e9
+            ach, des = hbm_figures(hb)
             blk["hbm_kernel"] = {"kernel": hb, "achieved": round(ach, 1),
-                                 "frac": round(ach / peak, 4),
+                                 "frac": round(ach / peak, 4), "frac_design": round(des / peak, 4),
                                  "traffic": ncu_traffic(cname, precision, hb),
-                                 "share_of_step": round(e["ms"] / step_ms, 4)}
+                                 "share_of_step": round(by_kernel[hb]["ms"] / step_ms, 4)}
     return blk
 
 
@@ -375,10 +394,15 @@ def time_precision(cfg, cname, precision, steps, warmup, world, rank, local, clo
     kernel_ms = plan.profile_kernels("exprk22", warmup + steps, n_prof)
     cells = cfg.N_rho * cfg.N_theta
     total_members = ENSEMBLE_MEMBERS if cname == "c4" else world
+    value = total_members * cells * steps / (ms_max * 1e-3)
+    roof = roofline_block(cfg, cname, precision, kernel_ms, n_prof, len(members))
+    # whole step against SURVEY 8(d)'s 16F per cell-step (128 B fp64, 64 B fp32)
+    per_cell = 16 * (8 if precision == "double" else 4)
+    roof["step_frac_16F"] = round(value / world * per_cell / (roof["peak"] * 1e9), 4)
     res = {
-        "value": total_members * cells * steps / (ms_max * 1e-3),
+        "value": value,
         "ms_per_step": ms_max / steps,
-        "roofline": roofline_block(cfg, cname, precision, kernel_ms, n_prof, len(members)),
+        "roofline": roof,
         "max_abs_v_last": float(max_abs[0, -1]),
         "clocks": sampler.summary() if clocks else None,
         "plan_bytes": plan.bytes,
@@ -415,43 +439,54 @@ def time_slab(cfg, steps, warmup, world, rank, local):
 
 
 def e2e_precision(cfg, cname, precision, steps, world, rank, local):
-    """Same metric through the public API with host buffers (run_exprk22)."""
+    """The same metric end to end through the public API with host buffers.
+
+    Single grids: ``run_exprk22(config, v0, fields)`` -- exactly the
+    reference's call (``nwave/exprk.py:219-224``: full N_sigma march, default
+    per-step timing buckets, numpy in and out) for fp64; ``precision=`` is the
+    one extra keyword for fp32.  The timed region holds the plan build (device
+    tables), the H2D of V0 and of the N_sigma + 1 coefficient rows, the whole
+    march and the D2H of the float64 final field.  C4: ``run_ensemble`` over
+    this rank's members, full length, final fields back to the host.
+    """
     import torch
     import paper_2103_06080_b200 as nw
 
     members = members_for(cname, world, rank)
     v0 = initial_fields(cfg, cname, members)
-    fields = coefficient_fields(cfg, cname, steps + 1)
+    n_full = cfg.N_sigma
+    fields = coefficient_fields(cfg, cname, n_full + 1)
+    kw = {} if precision == "double" else {"precision": precision}
     if cname != "c4":
-        # untimed warm-up call (3 steps): CUDA graph capture, the device memory pool
-        # and the page-locked result block are set up as in any repeated use
-        nw.run_exprk22(cfg, nw.Field2D(v0[0]), fields, precision=precision, max_steps=3,
-                       timing=False, device=torch.device("cuda", local))
+        # untimed warm-up call (3 steps): CUDA graph capture, the device memory
+        # pool and the page-locked staging chunks are set up as in any repeated use
+        nw.run_exprk22(cfg, nw.Field2D(v0[0]), fields, max_steps=3, **kw)
     torch.cuda.synchronize(local)
     barrier(world)
     t0 = time.perf_counter()
     if cname == "c4":
         from paper_2103_06080_b200.ensemble import run_ensemble
 
-        res = run_ensemble(cfg, v0, fields, precision=precision, max_steps=steps,
+        res = run_ensemble(cfg, v0, fields, precision=precision,
                            members=range(0, len(members)), device=torch.device("cuda", local))
         final = res.final
+        call = "run_ensemble(config, v0s, fields) over this rank's members"
     else:
-        rep = nw.run_exprk22(cfg, nw.Field2D(v0[0]), fields, precision=precision,
-                             max_steps=steps, timing=False, device=torch.device("cuda", local))
+        rep = nw.run_exprk22(cfg, nw.Field2D(v0[0]), fields, **kw)
         final = rep.final.values
+        assert rep.n_steps == n_full
+        call = "run_exprk22(config, v0, fields)" + ("" if not kw else ", precision='single'")
     wall = time.perf_counter() - t0
     wall_max = max_over_ranks(wall, world)
-    r = 8 if precision == "double" else 4
-    h2d = v0.size * 8 + 3 * (steps + 1) * cfg.N_rho * 8
-    d2h = final.size * 8 + 8 * steps * len(members)
+    h2d = v0.size * 8 + 3 * (n_full + 1) * cfg.N_rho * 8
+    d2h = final.size * 8 + 8 * n_full * len(members)
     total = ENSEMBLE_MEMBERS if cname == "c4" else world
-    return {"value": total * cfg.N_rho * cfg.N_theta * steps / wall_max, "unit": UNIT,
-            "h2d_bytes_per_step": int(h2d / steps), "d2h_bytes_per_step": int(d2h / steps),
-            "wall_s": wall_max, "steps": steps,
-            "note": "run_exprk22(numpy v0, numpy fields) incl. plan build, H2D, D2H of the "
-                    f"float64 final field; working precision {r * 8}-bit; after one untimed "
-                    "3-step warm-up call"}
+    return {"value": total * cfg.N_rho * cfg.N_theta * n_full / wall_max, "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d / n_full), "d2h_bytes_per_step": int(d2h / n_full),
+            "wall_s": wall_max, "steps": n_full, "precision": precision,
+            "note": f"{call}: the full N_sigma = {n_full}-step run with numpy inputs and "
+                    "outputs; timed region = plan build + H2D (V0, coefficient rows) + march + "
+                    "D2H of the float64 final field, after one untimed 3-step warm-up call"}
 
 
 def cpu_reference(cfg, cname, steps_cap=3, warm=1, threads=0, precision="double"):
@@ -540,9 +575,11 @@ def main():
     res32 = None
     if not args.no_fp32:
         res32 = time_precision(cfg, args.config, "single", args.steps, warmup, world, rank, local)
-    e2e = None
+    e2e = e2e32 = None
     if not args.no_e2e:
         e2e = e2e_precision(cfg, args.config, "double", args.steps, world, rank, local)
+        if res32 is not None:
+            e2e32 = e2e_precision(cfg, args.config, "single", args.steps, world, rank, local)
     cpu = None
     if world == 1 and not args.no_cpu:
         cpu = cpu_reference(cfg, args.config)
@@ -559,7 +596,8 @@ def main():
                          if cpu else None),
         "clocks": res64["clocks"],
         "fp32": ({"value": res32["value"], "ms_per_step": res32["ms_per_step"],
-                  "roofline": res32["roofline"], "clocks": res32["clocks"]} if res32 else None),
+                  "roofline": res32["roofline"], "clocks": res32["clocks"],
+                  "e2e": e2e32} if res32 else None),
         "impl": "b200",
     }
     print(json.dumps(line), flush=True)

@@ -279,3 +279,49 @@ def march(config, v0, fields, scheme="exprk22", precision="double", threads=0,
     if n_steps in plan:
         snaps[plan[n_steps]] = final.copy()
     return OracleRun(final, max_abs, snaps, secs, tr.count - 1, failed)
+
+
+@dataclass
+class OracleBatchRun:
+    final: np.ndarray          # (M, N_rho, N_theta) float64
+    max_abs_v: np.ndarray      # per member
+    transforms: int
+
+
+def march_batch(config, v0s, fields, scheme="exprk22", precision="double", threads=0,
+                max_steps=None) -> OracleBatchRun:
+    """``march`` for M independent members sharing grid, tables and coefficients
+    (BASELINE C4).  Per member the arithmetic is the reference's
+    (``exprk.py:151-178,219-331``): scipy's rfft2/irfft2 over the last two axes
+    transform every member on its own, WENO runs member by member, the combines
+    are the same elementwise numpy expressions.  The tables are built once.
+    """
+    workers = threads if threads > 0 else host_cores()
+    nr, nt = config.N_rho, config.N_theta
+    n_steps = config.N_sigma if max_steps is None else min(config.N_sigma, max_steps)
+    rdt = np.float64 if precision == "double" else np.float32
+    cdt = np.complex128 if precision == "double" else np.complex64
+    eps = EPS_DOUBLE if precision == "double" else EPS_SINGLE
+    tabs = build_tables(nr, nt, config.rho_span, config.theta_span, config.d_sigma,
+                        config.A, eps, cdt)
+    rows = [np.ascontiguousarray(getattr(fields, name)[:, :nr], dtype=rdt)
+            for name in ("u_par", "u_perp", "du_perp_drho")]
+    d_sigma, b_coef = rdt(config.d_sigma), rdt(config.B)
+    v0s = np.ascontiguousarray(v0s, dtype=rdt)
+    tr = Transforms((nr, nt), workers)
+    vhat = tr.forward(v0s)
+    tr.count = 0
+    step = step_exprk22 if scheme == "exprk22" else step_expeuler
+    max_abs = np.zeros(len(v0s))
+    for n in range(n_steps):
+        def b_eval(stage, v, _row=n):
+            r = _row + stage
+            return np.stack([weno5_b(v[i], rows[0][r], rows[1][r], rows[2][r], b_coef,
+                                     config.d_rho, config.d_theta, workers)
+                             for i in range(len(v))])
+        vhat, v_n = step(vhat, tabs, b_eval, d_sigma, tr)
+        max_abs = np.maximum(max_abs, np.max(np.abs(v_n), axis=(1, 2)))
+    v_fin = tr.inverse(vhat)
+    max_abs = np.maximum(max_abs, np.max(np.abs(v_fin), axis=(1, 2)))
+    return OracleBatchRun(np.asarray(v_fin, np.float64), max_abs.astype(np.float64),
+                          tr.count - 1)

@@ -51,8 +51,14 @@ def _sources():
     return deps
 
 
+STAMP = LIB_PATH + ".defines"
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB_PATH):
+        return False
+    # a library built with experiment defines is never the default build
+    if os.path.exists(STAMP) and open(STAMP).read().strip():
         return False
     t = os.path.getmtime(LIB_PATH)
     return all(os.path.getmtime(d) <= t for d in _sources())
@@ -60,7 +66,10 @@ def up_to_date() -> bool:
 
 def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
           defines=(), out: str | None = None) -> str:
-    """Compile and link; ``defines``/``out`` build an experiment variant."""
+    """Compile and link; ``defines`` build an experiment variant, which must be
+    written elsewhere (``out``) so the default library is never a variant."""
+    if defines and out is None:
+        raise ValueError("experiment defines need an explicit out= library path")
     lib_path = out or LIB_PATH
     if not force and not defines and out is None and up_to_date():
         return LIB_PATH
@@ -100,6 +109,8 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, lib_path)
+    with open(lib_path + ".defines", "w") as fh:
+        fh.write(" ".join(defines))
     return lib_path
 
 

@@ -136,7 +136,23 @@ def last_error() -> str:
     return raw.decode(errors="replace") if raw else ""
 
 
-def check(rc: int, what: str = ""):
+def instability_from_message(msg: str, d_sigma: float | None = None) -> InstabilityError:
+    """InstabilityError(sigma, max_abs) from the library's guard message
+    (``step=<n> member=<i> max_abs=<v>``): sigma = n * d_sigma like the
+    reference (``exprk.py:297-299``); nan when the step size is not known."""
+    import re
+
+    fields = dict(re.findall(r"(step|member|max_abs)=(\S+)", msg))
+    step = int(fields["step"]) if "step" in fields else None
+    value = float(fields["max_abs"]) if "max_abs" in fields else float("nan")
+    sigma = step * d_sigma if (step is not None and d_sigma is not None) else float("nan")
+    err = InstabilityError(sigma, value)
+    err.step = step
+    err.member = int(fields["member"]) if "member" in fields else None
+    return err
+
+
+def check(rc: int, what: str = "", d_sigma: float | None = None):
     if rc == NWB_OK:
         return
     msg = f"{what}: {last_error()}" if what else last_error()
@@ -145,7 +161,7 @@ def check(rc: int, what: str = ""):
     if rc == NWB_EUNSUPPORTED:
         raise UnsupportedSizeError(msg)
     if rc == NWB_EINSTABILITY:
-        raise InstabilityError(float("nan"), float("nan"))
+        raise instability_from_message(msg, d_sigma)
     if rc == NWB_EBUDGET:
         raise BudgetExceededError(msg)
     raise BackendError(f"{msg} (code {rc})")

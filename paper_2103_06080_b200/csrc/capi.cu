@@ -300,6 +300,16 @@ struct nwb_plan {
   // graphs (one captured step per scheme)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   cudaStream_t graph_stream[2] = {nullptr, nullptr};
+  // timed graphs: the same step with external event-record nodes at the stage
+  // bucket boundaries; each replay points the nodes at that step's events
+  // (cudaGraphExecEventRecordNodeSetEvent), so the drop-in default path
+  // (per-step nonlinear / linear buckets) still runs from a CUDA graph
+  cudaGraph_t tgraph_g[2] = {nullptr, nullptr};
+  cudaGraphExec_t tgraph[2] = {nullptr, nullptr};
+  cudaStream_t tgraph_stream[2] = {nullptr, nullptr};
+  cudaGraphNode_t tnode[2][10] = {};
+  cudaEvent_t tev[10] = {};          // placeholder events recorded during capture
+  bool ev_external = false;          // capturing: record events as external nodes
   std::vector<void*> allocs;
 };
 
@@ -412,10 +422,15 @@ template <typename T> WenoArgs<T> weno_args(const nwb_plan* p) {
 // ev (optional) holds 5 events: before c2r and after each of the 4 kernels.
 constexpr int EV_PER_STAGE = 5;
 
+inline void rec_event(const nwb_plan* p, cudaEvent_t e, cudaStream_t s) {
+  if (p->ev_external) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else cudaEventRecord(e, s);
+}
+
 template <typename T>
 void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   cudaStream_t s = p->stream;
-  if (ev) cudaEventRecord(ev[0], s);
+  if (ev) rec_event(p, ev[0], s);
   // theta c2r of T (stage 1) or T* (stage 2) into v
   ThetaArgs<T> c = theta_args<T>(p);
   c.spec_in = (const cplx<T>*)(stage == 1 ? p->t : p->ts);
@@ -426,7 +441,7 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   c.alpha_bits = p->red + (stage - 1);
   c.vmax_bits = stage == 1 ? p->vmax_hist : nullptr;
   launch_theta_c2r<T>(c, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows_c2r, s);
-  if (ev) cudaEventRecord(ev[1], s);
+  if (ev) rec_event(p, ev[1], s);
   // WENO -> b
   WenoArgs<T> w = weno_args<T>(p);
   w.step_ctr = p->step_ctr;
@@ -456,10 +471,10 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
     cudaStreamWaitEvent(s, p->ov_ev[8], 0);
   } else {
     launch_weno<T>(w, s);
-    if (ev) cudaEventRecord(ev[2], s);
+    if (ev) rec_event(p, ev[2], s);
     launch_theta_r2c<T>(r, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
   }
-  if (ev) cudaEventRecord(ev[3], s);
+  if (ev) rec_event(p, ev[3], s);
   // rho pass
   RhoArgs<T> q = rho_args<T>(p);
   q.in = (const cplx<T>*)p->bt;
@@ -480,13 +495,24 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
     q.zero_bits = p->red + 0;
   }
   launch_rho<T>(q, mode, p->rho_threads, s);
-  if (ev) cudaEventRecord(ev[4], s);
+  if (ev) rec_event(p, ev[4], s);
 }
 
 // ev (optional): 2 * EV_PER_STAGE events
 template <typename T> void launch_step(nwb_plan* p, int scheme, cudaEvent_t* ev) {
   launch_stage<T>(p, 1, scheme, ev);
   if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev ? ev + EV_PER_STAGE : nullptr);
+}
+
+void drop_graphs(nwb_plan* p) {
+  for (int i = 0; i < 2; ++i) {
+    if (p->graph[i]) cudaGraphExecDestroy(p->graph[i]);
+    if (p->tgraph[i]) cudaGraphExecDestroy(p->tgraph[i]);
+    if (p->tgraph_g[i]) cudaGraphDestroy(p->tgraph_g[i]);
+    p->graph[i] = nullptr;
+    p->tgraph[i] = nullptr;
+    p->tgraph_g[i] = nullptr;
+  }
 }
 
 // per-step guard history [batch][len]; reallocation invalidates captured graphs
@@ -497,11 +523,7 @@ int ensure_hist(nwb_plan* p, int len) {
   p->hist_len = len;
   TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)p->g.batch * len * sizeof(u64)));
   CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)p->g.batch * len * sizeof(u64), p->stream));
-  for (int i = 0; i < 2; ++i)
-    if (p->graph[i]) {
-      cudaGraphExecDestroy(p->graph[i]);
-      p->graph[i] = nullptr;
-    }
+  drop_graphs(p);
   return NWB_OK;
 }
 
@@ -621,11 +643,7 @@ template <typename T> int set_coeffs_impl(nwb_plan* p, const double* up, const d
   TRY(dalloc(p, &p->du, n * sizeof(T)));
   TRY(dalloc(p, (void**)&p->alpha_rho, (size_t)n_rows * sizeof(double)));
   p->n_rows = n_rows;
-  for (int i = 0; i < 2; ++i)  // captured steps point at the old coefficient buffers
-    if (p->graph[i]) {
-      cudaGraphExecDestroy(p->graph[i]);
-      p->graph[i] = nullptr;
-    }
+  drop_graphs(p);  // captured steps point at the old coefficient buffers
   TRY(ensure_hist(p, n_rows));
   double* stage = nullptr;
   CU(cudaMallocAsync(&stage, n * sizeof(double), p->stream));
@@ -786,6 +804,59 @@ template <typename T> int graph_for(nwb_plan* p, int scheme) {
   return NWB_OK;
 }
 
+// The timed step graph: launch_step with external event-record nodes at the
+// 2 x EV_PER_STAGE bucket boundaries (placeholder events p->tev); the nodes
+// are kept (in capture order) so march_impl can point them at per-step events.
+template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
+  const int gi = scheme == NWB_SCHEME_EXPRK22 ? 0 : 1;
+  if (p->tgraph[gi] && p->tgraph_stream[gi] == p->stream) return NWB_OK;
+  if (p->tgraph[gi]) cudaGraphExecDestroy(p->tgraph[gi]);
+  if (p->tgraph_g[gi]) cudaGraphDestroy(p->tgraph_g[gi]);
+  p->tgraph[gi] = nullptr;
+  p->tgraph_g[gi] = nullptr;
+  for (auto& e : p->tev)
+    if (!e) CU(cudaEventCreate(&e));
+  cudaGraph_t gr;
+  CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  p->ev_external = true;
+  launch_step<T>(p, scheme, p->tev);
+  p->ev_external = false;
+  cudaError_t le = cudaGetLastError();
+  CU(cudaStreamEndCapture(p->stream, &gr));
+  if (le != cudaSuccess) {
+    cudaGraphDestroy(gr);
+    return fail(NWB_ECUDA, std::string("timed graph capture: ") + cudaGetErrorString(le));
+  }
+  size_t nn = 0;
+  CU(cudaGraphGetNodes(gr, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CU(cudaGraphGetNodes(gr, nodes.data(), &nn));
+  const int nev = (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1) * EV_PER_STAGE;
+  int found = 0;
+  for (int i = 0; i < nev; ++i) p->tnode[gi][i] = nullptr;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    CU(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t e;
+    CU(cudaGraphEventRecordNodeGetEvent(nd, &e));
+    for (int i = 0; i < nev; ++i)
+      if (p->tev[i] == e && !p->tnode[gi][i]) {
+        p->tnode[gi][i] = nd;
+        ++found;
+        break;
+      }
+  }
+  if (found != nev) {
+    cudaGraphDestroy(gr);
+    return fail(NWB_ECUDA, "timed graph: event-record nodes not found");
+  }
+  CU(cudaGraphInstantiate(&p->tgraph[gi], gr, 0));
+  p->tgraph_g[gi] = gr;
+  p->tgraph_stream[gi] = p->stream;
+  return NWB_OK;
+}
+
 template <typename T>
 int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, double max_seconds,
                const int* snap_steps, int n_snap, void* const* snap_bufs, double* max_abs,
@@ -801,8 +872,10 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
   CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)g.batch * p->hist_len * sizeof(u64), p->stream));
   CU(cudaMemsetAsync(p->red, 0, (size_t)g.batch * 4 * sizeof(u64), p->stream));
   TRY(set_step(p, n0));
-  const bool use_graph = step_ms == nullptr;
-  if (use_graph) TRY(graph_for<T>(p, scheme));
+  const int gi = scheme == NWB_SCHEME_EXPRK22 ? 0 : 1;
+  if (step_ms) TRY(timed_graph_for<T>(p, scheme));
+  else TRY(graph_for<T>(p, scheme));
+  const int nev = (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1) * EV_PER_STAGE;
 
   std::vector<cudaEvent_t> evs;
   if (step_ms) {
@@ -814,24 +887,38 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
     evs.clear();
   };
   const auto t_start = std::chrono::steady_clock::now();
-  const int chunk = max_seconds > 0 ? 8 : 64;
+  // budget (max_seconds >= 0; negative = none): checked after every chunk; the
+  // first chunk is one step so a zero budget stops after step 1 like the
+  // reference (exprk.py:303-306), later chunks are 8 steps
+  const bool budget = max_seconds >= 0;
   std::vector<u64> hbuf;
   int rc = NWB_OK;
   int done = 0;
   while (done < n_steps && rc == NWB_OK) {
+    const int chunk = budget ? (done == 0 ? 1 : 8) : 64;
     const int cnt = std::min(chunk, n_steps - done);
     for (int i = 0; i < cnt; ++i) {
       const int n = n0 + done + i;
       int snap = -1;
       for (int q = 0; q < n_snap; ++q)
         if (snap_steps[q] == n) snap = q;
-      if (step_ms) {
+      if (step_ms && snap >= 0) {
         cudaEvent_t* ev = &evs[(size_t)(done + i) * 2 * EV_PER_STAGE];
         launch_stage<T>(p, 1, scheme, ev);
-        if (snap >= 0)
-          cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
-                          cudaMemcpyDeviceToDevice, p->stream);
+        cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
+                        cudaMemcpyDeviceToDevice, p->stream);
         if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev + EV_PER_STAGE);
+      } else if (step_ms) {
+        // replay the timed graph with its event nodes pointed at this step's events
+        cudaEvent_t* ev = &evs[(size_t)(done + i) * 2 * EV_PER_STAGE];
+        cudaError_t e = cudaSuccess;
+        for (int q = 0; q < nev && e == cudaSuccess; ++q)
+          e = cudaGraphExecEventRecordNodeSetEvent(p->tgraph[gi], p->tnode[gi][q], ev[q]);
+        if (e == cudaSuccess) e = cudaGraphLaunch(p->tgraph[gi], p->stream);
+        if (e != cudaSuccess) {
+          destroy_events();
+          return fail(NWB_ECUDA, std::string("timed graph launch: ") + cudaGetErrorString(e));
+        }
       } else if (snap >= 0) {
         launch_stage<T>(p, 1, scheme, nullptr);
         cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
@@ -869,15 +956,18 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
           if (fail_step) *fail_step = n0 + done + i;
           if (fail_member) *fail_member = mbr;
           if (fail_value) *fail_value = m;
-          rc = fail(NWB_EINSTABILITY, "max|V| left the guard");
+          char msg[160];
+          std::snprintf(msg, sizeof msg, "max|V| left the guard: step=%d member=%d max_abs=%.17g",
+                        n0 + done + i, mbr, m);
+          rc = fail(NWB_EINSTABILITY, msg);
           break;
         }
       }
     }
     done += cnt;
-    if (rc == NWB_OK && max_seconds > 0) {
+    if (rc == NWB_OK && budget) {
       const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
-      if (el > max_seconds && done < n_steps) {
+      if (el > max_seconds) {
         if (fail_step) *fail_step = n0 + done;
         rc = fail(NWB_EBUDGET, "wall-clock budget exhausted");
       }
@@ -1413,8 +1503,9 @@ int nwb_plan_destroy(nwb_plan* p) {
   if (!p) return NWB_OK;
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->stream);
-  for (int i = 0; i < 2; ++i)
-    if (p->graph[i]) cudaGraphExecDestroy(p->graph[i]);
+  drop_graphs(p);
+  for (cudaEvent_t e : p->tev)
+    if (e) cudaEventDestroy(e);
   for (void* a : p->allocs)
     if (a) cudaFreeAsync(a, p->stream);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);

@@ -88,7 +88,12 @@ def run_ensemble(config: DomainConfig, v0s, fields, scheme: str = "exprk22",
         gm = ground_metrics_device(config, v_fin, trace_rho, stream=plan.stream)
         peak = np.array([g.peak for g in gm])
         rise = np.array([g.rise_theta for g in gm])
-        final = v_fin.to("cpu", torch.float64).numpy() if keep_fields else None
+        if keep_fields:  # staged through reusable page-locked chunks (hostio)
+            from .hostio import to_host64
+
+            final = to_host64(v_fin, plan.stream)
+        else:
+            final = None
     finally:
         plan.close()
     mabs = np.maximum(max_abs.max(axis=1) if n_steps else 0.0, mx)

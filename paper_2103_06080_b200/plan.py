@@ -195,12 +195,19 @@ class DevicePlan:
 
     # ------------------------------------------------------------ march
     def march(self, scheme: str, n0: int, n_steps: int, guard: float = 10.0,
-              max_seconds: float | None = None, snap_steps=(), timing: bool = True):
+              max_seconds: float | None = None, snap_steps=(), timing: bool = True,
+              total_steps: int | None = None):
         """Advance the device state; returns (max_abs[batch, n_steps],
         step_ms[n_steps, 3] or None, {step: device snapshot}).
 
+        Both modes replay a captured CUDA graph per step; ``timing`` adds the
+        per-step bucket events (nonlinear = WENO + theta r2c, rest linear).
+        ``snap_steps`` inside the range are copied to fresh device buffers
+        (run_exprk22 streams its snapshots instead, see ``SnapshotStreamer``).
         Raises InstabilityError with the reference's sigma = n * d_sigma of the
-        first offending step, BudgetExceededError when out of wall clock.
+        first offending step, BudgetExceededError when out of wall clock
+        (``max_seconds`` counted from this call; the message numbers steps out
+        of ``total_steps``, default n0 + n_steps).
         """
         torch = _torch()
         code = _lib.SCHEME_EXPRK22 if scheme == "exprk22" else _lib.SCHEME_EXPEULER
@@ -215,7 +222,7 @@ class DevicePlan:
             ptrs_arr = (ctypes.c_void_p * max(len(snaps), 1))(*[bufs[s].data_ptr() for s in snaps])
             rc = self.lib.nwb_march(
                 self._h, code, int(n0), int(n_steps), float(guard),
-                float(max_seconds) if max_seconds is not None else 0.0,
+                float(max_seconds) if max_seconds is not None else -1.0,
                 steps_arr, len(snaps), ptrs_arr, max_abs.ctypes.data_as(ctypes.c_void_p),
                 step_ms.ctypes.data_as(ctypes.c_void_p) if step_ms is not None else None,
                 ctypes.byref(fail_step), ctypes.byref(fail_member), ctypes.byref(fail_value))
@@ -227,11 +234,17 @@ class DevicePlan:
         if rc == _lib.NWB_EBUDGET:
             from .errors import BudgetExceededError
 
-            done = fail_step.value - n0
+            total = total_steps if total_steps is not None else n0 + n_steps
             raise BudgetExceededError(
-                f"exceeded {max_seconds:.0f} s at step {done}/{n_steps}")
-        check(rc, "nwb_march")
+                f"exceeded {max_seconds:.0f} s at step {fail_step.value}/{total}")
+        check(rc, "nwb_march", d_sigma=self.d_sigma)
         return max_abs, step_ms, bufs
+
+    def store_physical_into(self, out):
+        """c2r of the state into ``out`` (batch, n_rho, n_theta) on the plan
+        stream (same kernel as the stage-1 c2r: bitwise the step-start field)."""
+        with self.on_stream():
+            check(self.lib.nwb_plan_store_physical(self._h, ptr(out), None), "store_physical")
 
     def profile_kernels(self, scheme: str, n0: int, n_steps: int) -> np.ndarray:
         """Summed device ms per kernel slot over n_steps steps (CUDA events

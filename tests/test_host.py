@@ -71,6 +71,24 @@ def test_error_mapping():
     assert issubclass(nw.UnsupportedSizeError, nw.BackendError)
 
 
+def test_instability_message_carries_sigma():
+    from paper_2103_06080_b200._lib import instability_from_message
+
+    e = instability_from_message("nwb_march: max|V| left the guard: step=7 member=3 "
+                                 "max_abs=12.5", d_sigma=0.25)
+    assert isinstance(e, nw.InstabilityError)
+    assert e.sigma == 1.75 and e.max_abs == 12.5 and e.step == 7 and e.member == 3
+    e = instability_from_message("max|V| left the guard: step=2 member=0 max_abs=nan")
+    assert np.isnan(e.sigma) and np.isnan(e.max_abs) and e.step == 2
+
+
+def test_variant_build_needs_explicit_output():
+    from paper_2103_06080_b200 import _build
+
+    with pytest.raises(ValueError):
+        _build.build(defines=("NWB_WENO_WALK=0",))
+
+
 def test_domain_config_validation_and_spacings():
     c = nw.DomainConfig()
     assert c.N_rho == 1250 and c.N_theta == 448 and c.N_sigma == 300
@@ -174,16 +192,21 @@ def test_bench_roofline_bookkeeping():
     spec = cfg.N_rho * (cfg.N_theta // 2 + 1) * 16
     # tables read at canonical +-f positions: 60 % of each row at N_rho = 10000 (r1 = 5)
     assert bench.table_read_fraction(cfg.N_rho) == pytest.approx(0.6)
-    assert b[1] == 2 * F and b[3] == 4 * spec + int(1.8 * spec) and b[7] == 4 * spec + int(0.6 * spec)
+    # SURVEY 8(d) algorithmic bytes: 2F per theta / WENO launch, 4F per rho launch
+    assert b[0] == spec + F and b[1] == 2 * F and b[2] == F + spec
+    assert b[3] == 4 * spec and b[7] == 4 * spec
+    d = bench.algorithmic_bytes(cfg, "double", design=True)
+    assert d[3] == 4 * spec + int(1.8 * spec) and d[7] == 4 * spec + int(0.6 * spec)
     blk = bench.roofline_block(cfg, "c2", "double", [1.0, 2.0, 1.0, 3.0, 1.0, 2.0, 1.0, 2.5], 1)
     # both rho stages are one kernel (k_rho): 5.5 ms beats WENO's 4 ms
     assert blk["kernel"] == "rho_pass" and blk["unit"] == "GB/s"
     assert blk["achieved"] == pytest.approx((b[3] + b[7]) / 5.5e-3 / 1e9, rel=1e-3)
-    assert 0 < blk["frac"] < 10
+    assert blk["achieved_design"] == pytest.approx((d[3] + d[7]) / 5.5e-3 / 1e9, rel=1e-3)
+    assert 0 < blk["frac"] < blk["frac_design"] < 10
     blk = bench.roofline_block(cfg, "c2", "double", [1.0, 4.0, 1.0, 1.0, 1.0, 4.0, 1.0, 1.0], 1)
     assert blk["kernel"] == "weno"
     # tables are shared by the members of a batch
-    b4 = bench.algorithmic_bytes(cfg, "double", 4)
+    b4 = bench.algorithmic_bytes(cfg, "double", 4, design=True)
     assert b4[3] == 4 * 4 * spec + int(1.8 * spec) and b4[1] == 4 * 2 * F
 
 

@@ -127,3 +127,25 @@ def test_turbulence_host_restatement(golden):
     got = np.stack([f.u_par, f.u_perp, f.du_perp_dsigma, f.du_perp_drho])
     ref = golden["turb_small"]
     assert np.max(np.abs(got - ref)) <= 1e-15 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_march_batch_equals_member_marches(oracle, precision):
+    """The batched oracle march (used to check the 256-member C4 GPU run) is the
+    per-member march, bitwise: every member is transformed and WENO'd on its own."""
+    from paper_2103_06080_b200.analysis import ensemble_nwaves
+    from paper_2103_06080_b200.grid import rho_nodes_closed
+    from paper_2103_06080_b200.turbulence import (TurbulenceParams, evaluate_fields,
+                                                  sample_modes)
+
+    c = DomainConfig(N_rho=40, N_theta=56, N_sigma=5, Sigma=2.0)
+    sig, _, _ = build_axes(c)
+    spec = sample_modes(TurbulenceParams(seed=0))
+    f = evaluate_fields(spec, spec.lam, sig, rho_nodes_closed(c))
+    v0s, _, _ = ensemble_nwaves(c, 3, seed=2026)
+    run = oracle.march_batch(c, v0s, f, precision=precision)
+    assert run.transforms == 4 * c.N_sigma
+    for i in range(3):
+        one = oracle.march(c, v0s[i], f, precision=precision)
+        assert np.array_equal(run.final[i], one.final)
+        assert run.max_abs_v[i] == one.max_abs_v
