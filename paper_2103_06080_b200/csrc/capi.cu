@@ -50,7 +50,9 @@ struct FftPlanHost {
   std::vector<std::pair<int, int>> passes;  // (ra, rb)
 };
 
-bool plan_fft(int n, bool split_two, FftPlanHost& h, int max_prod = 16) {
+// first > 1 forces a lone first stage of that radix (2, 3, 4, 5, 7): the
+// cluster-split rho pass (2) and the theta-fused first rho stage (r1).
+bool plan_fft(int n, int first, FftPlanHost& h, int max_prod = 16) {
   int m = n, c2 = 0, c3 = 0, c5 = 0, c7 = 0;
   while (m % 2 == 0) { m /= 2; ++c2; }
   while (m % 3 == 0) { m /= 3; ++c3; }
@@ -59,10 +61,13 @@ bool plan_fft(int n, bool split_two, FftPlanHost& h, int max_prod = 16) {
   if (m != 1) return false;
   const bool big = max_prod >= 16;  // 16: pair 7.2, 5.3, 5.2, 3.4, 3.3, 4.4; 8: only 3.2 and 8
   std::vector<std::pair<int, int>> ps;
-  if (split_two) {
-    if (c2 == 0) return false;
-    ps.push_back({2, 1});
-    --c2;
+  const bool split_two = first > 1;
+  if (first > 1) {
+    int* cnt = first == 2 || first == 4 ? &c2 : first == 3 ? &c3 : first == 5 ? &c5 : first == 7 ? &c7 : nullptr;
+    const int need = first == 4 ? 2 : 1;
+    if (!cnt || *cnt < need) return false;
+    ps.push_back({first, 1});
+    *cnt -= need;
   }
   for (; c7 > 0; --c7) {
     if (big && c2 > 0) { ps.push_back({7, 2}); --c2; } else ps.push_back({7, 1});
@@ -280,6 +285,11 @@ struct nwb_plan {
   int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
   int rho_ws = 0, rho_ws2 = 0, rho_ws_ctas = 0;  // warp-specialised rho pass (k_rho_ws) group sizes, CTAs
   void* ws_scratch = nullptr;
+  // first rho stage fused into the theta passes (r1 > 1): rho CTAs own
+  // msub = nr / r1 point sub-columns (dsub / tw_sub); tw_first = W_nr^t
+  int rho_r1 = 1, msub = 0;
+  FftDesc dsub{};
+  void *tw_sub = nullptr, *tw_first = nullptr;
   FftDesc dh2{};             // half-column descriptor (split mode)
   void *tw_h2 = nullptr, *tw_split = nullptr;
   size_t rsz = 8;  // sizeof(real)
@@ -304,8 +314,12 @@ struct nwb_plan {
   // bucket boundaries; each replay points the nodes at that step's events
   // (cudaGraphExecEventRecordNodeSetEvent), so the drop-in default path
   // (per-step nonlinear / linear buckets) still runs from a CUDA graph
+  // NTG instances per scheme are replayed round robin: an instance's event nodes
+  // are re-pointed only after its previous replay has finished (re-pointing a
+  // node whose replay is still in flight fails with cudaErrorInvalidValue)
+  static constexpr int NTG = 4;
   cudaGraph_t tgraph_g[2] = {nullptr, nullptr};
-  cudaGraphExec_t tgraph[2] = {nullptr, nullptr};
+  cudaGraphExec_t tgraph[2][NTG] = {};
   cudaStream_t tgraph_stream[2] = {nullptr, nullptr};
   cudaGraphNode_t tnode[2][10] = {};
   cudaEvent_t tev[10] = {};          // placeholder events recorded during capture
@@ -368,6 +382,9 @@ template <typename T> ThetaArgs<T> theta_args(const nwb_plan* p) {
   a.alpha_stride = 4;
   a.vmax_stride = p->hist_len;
   a.debug = p->theta_debug;
+  a.r1 = p->rho_r1;
+  a.msub = p->msub;
+  a.tw_first = (const cplx<T>*)p->tw_first;
   return a;
 }
 
@@ -399,6 +416,10 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.dh2 = p->dh2;
   a.tw_h2 = (const cplx<T>*)p->tw_h2;
   a.tw_split = (const cplx<T>*)p->tw_split;
+  a.r1 = p->rho_r1;
+  a.dsub = p->dsub;
+  a.tw_sub = (const cplx<T>*)p->tw_sub;
+  a.rev_r = p->rev_r;
   return a;
 }
 
@@ -507,10 +528,12 @@ template <typename T> void launch_step(nwb_plan* p, int scheme, cudaEvent_t* ev)
 void drop_graphs(nwb_plan* p) {
   for (int i = 0; i < 2; ++i) {
     if (p->graph[i]) cudaGraphExecDestroy(p->graph[i]);
-    if (p->tgraph[i]) cudaGraphExecDestroy(p->tgraph[i]);
+    for (auto& x : p->tgraph[i]) {
+      if (x) cudaGraphExecDestroy(x);
+      x = nullptr;
+    }
     if (p->tgraph_g[i]) cudaGraphDestroy(p->tgraph_g[i]);
     p->graph[i] = nullptr;
-    p->tgraph[i] = nullptr;
     p->tgraph_g[i] = nullptr;
   }
 }
@@ -612,6 +635,20 @@ template <typename T> int create_impl(nwb_plan* p) {
     TRY(dalloc(p, &p->tw_split, tws.size() * C));
     CU(cudaMemcpy(p->tw_h2, tw2.data(), tw2.size() * C, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(p->tw_split, tws.data(), tws.size() * C, cudaMemcpyHostToDevice));
+  }
+
+  if (p->rho_r1 > 1) {
+    // sub-column transform = the full plan without its leading radix-r1 stage
+    FftPlanHost sub;
+    sub.stages.assign(p->plan_r.stages.begin() + 1, p->plan_r.stages.end());
+    sub.passes.assign(p->plan_r.passes.begin() + 1, p->plan_r.passes.end());
+    std::vector<cplx<T>> tws;
+    build_desc<T>(p->msub, sub, p->dsub, tws);
+    auto twf = twiddles<T>(g.nr, g.nr);
+    TRY(dalloc(p, &p->tw_sub, tws.size() * C));
+    TRY(dalloc(p, &p->tw_first, twf.size() * C));
+    CU(cudaMemcpy(p->tw_sub, tws.data(), tws.size() * C, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(p->tw_first, twf.data(), twf.size() * C, cudaMemcpyHostToDevice));
   }
 
   // multiplier tables, digit-reversed rho order (exprk.py:111-131)
@@ -733,8 +770,18 @@ template <typename T> int rfft2_impl(nwb_plan* p, const void* in, void* out) {
   RhoArgs<T> q = rho_args<T>(p);
   q.in = (const cplx<T>*)p->bt;
   q.out = (cplx<T>*)p->ts;
-  launch_rho<T>(q, RHO_FWD_NAT, p->rho_threads, p->stream);
-  launch_transpose<T>(p->g, (const cplx<T>*)p->ts, (cplx<T>*)out, 1, p->stream);
+  if (p->rho_r1 > 1) {
+    // sub-column transforms in digit-reversed positions, then one permutation
+    launch_rho<T>(q, RHO_FWD_DR, p->rho_threads, p->stream);
+    q.in = (const cplx<T>*)p->ts;
+    q.out = (cplx<T>*)p->bt;
+    q.r1 = 1;
+    launch_rho<T>(q, RHO_REV2NAT, p->rho_threads, p->stream);
+    launch_transpose<T>(p->g, (const cplx<T>*)p->bt, (cplx<T>*)out, 1, p->stream);
+  } else {
+    launch_rho<T>(q, RHO_FWD_NAT, p->rho_threads, p->stream);
+    launch_transpose<T>(p->g, (const cplx<T>*)p->ts, (cplx<T>*)out, 1, p->stream);
+  }
   CHECK_LAUNCH("rfft2");
   return NWB_OK;
 }
@@ -809,10 +856,12 @@ template <typename T> int graph_for(nwb_plan* p, int scheme) {
 // are kept (in capture order) so march_impl can point them at per-step events.
 template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
   const int gi = scheme == NWB_SCHEME_EXPRK22 ? 0 : 1;
-  if (p->tgraph[gi] && p->tgraph_stream[gi] == p->stream) return NWB_OK;
-  if (p->tgraph[gi]) cudaGraphExecDestroy(p->tgraph[gi]);
+  if (p->tgraph[gi][0] && p->tgraph_stream[gi] == p->stream) return NWB_OK;
+  for (auto& x : p->tgraph[gi]) {
+    if (x) cudaGraphExecDestroy(x);
+    x = nullptr;
+  }
   if (p->tgraph_g[gi]) cudaGraphDestroy(p->tgraph_g[gi]);
-  p->tgraph[gi] = nullptr;
   p->tgraph_g[gi] = nullptr;
   for (auto& e : p->tev)
     if (!e) CU(cudaEventCreate(&e));
@@ -851,7 +900,7 @@ template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
     cudaGraphDestroy(gr);
     return fail(NWB_ECUDA, "timed graph: event-record nodes not found");
   }
-  CU(cudaGraphInstantiate(&p->tgraph[gi], gr, 0));
+  for (auto& x : p->tgraph[gi]) CU(cudaGraphInstantiate(&x, gr, 0));
   p->tgraph_g[gi] = gr;
   p->tgraph_stream[gi] = p->stream;
   return NWB_OK;
@@ -883,6 +932,16 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
     for (auto& e : evs) CU(cudaEventCreate(&e));
   }
   auto destroy_events = [&]() {
+    // point the timed graphs' event nodes back at the plan's placeholder events
+    // before the per-step events die (a node must never reference a destroyed
+    // event: re-pointing it later fails with cudaErrorInvalidValue)
+    if (step_ms) {
+      cudaStreamSynchronize(p->stream);
+      for (auto ex : p->tgraph[gi])
+        if (ex)
+          for (int q = 0; q < nev; ++q) cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], p->tev[q]);
+      cudaGetLastError();
+    }
     for (auto& e : evs) cudaEventDestroy(e);
     evs.clear();
   };
@@ -910,14 +969,25 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
         if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev + EV_PER_STAGE);
       } else if (step_ms) {
         // replay the timed graph with its event nodes pointed at this step's events
-        cudaEvent_t* ev = &evs[(size_t)(done + i) * 2 * EV_PER_STAGE];
+        const int st = done + i;
+        cudaEvent_t* ev = &evs[(size_t)st * 2 * EV_PER_STAGE];
+        cudaGraphExec_t ex = p->tgraph[gi][st % nwb_plan::NTG];
         cudaError_t e = cudaSuccess;
-        for (int q = 0; q < nev && e == cudaSuccess; ++q)
-          e = cudaGraphExecEventRecordNodeSetEvent(p->tgraph[gi], p->tnode[gi][q], ev[q]);
-        if (e == cudaSuccess) e = cudaGraphLaunch(p->tgraph[gi], p->stream);
+        // this instance last ran step st - NTG: wait for it (its last event)
+        // before re-pointing its nodes
+        if (st >= nwb_plan::NTG)
+          e = cudaEventSynchronize(evs[(size_t)(st - nwb_plan::NTG) * 2 * EV_PER_STAGE + nev - 1]);
+        int q = 0;
+        for (; q < nev && e == cudaSuccess; ++q)
+          e = cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], ev[q]);
+        const bool set_failed = e != cudaSuccess;
+        if (e == cudaSuccess) e = cudaGraphLaunch(ex, p->stream);
         if (e != cudaSuccess) {
+          cudaGetLastError();  // do not leave the error for a later launch check
           destroy_events();
-          return fail(NWB_ECUDA, std::string("timed graph launch: ") + cudaGetErrorString(e));
+          return fail(NWB_ECUDA, std::string(set_failed ? "timed graph event node " + std::to_string(q - 1)
+                                                        : std::string("timed graph launch")) +
+                                     " (step " + std::to_string(n) + "): " + cudaGetErrorString(e));
         }
       } else if (snap >= 0) {
         launch_stage<T>(p, 1, scheme, nullptr);
@@ -1245,7 +1315,7 @@ int nwb_slab_create(nwb_slab** out, int n_rho, int n_theta, int j0, int rows, in
   s->k0 = k0; s->modes = modes; s->ld_rho = (n_rho + 7) / 8 * 8;
   s->d_sigma = d_sigma; s->rho_span = rho_span; s->theta_span = theta_span;
   s->A = A; s->B = B; s->eps = eps;
-  if (!plan_fft(n_rho, false, s->plan_r) || !plan_fft(s->m, false, s->plan_h)) {
+  if (!plan_fft(n_rho, 0, s->plan_r) || !plan_fft(s->m, 0, s->plan_h)) {
     delete s;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
   }
@@ -1401,10 +1471,23 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
       }
     }
   }
+  // First rho stage fused into the theta passes (NWB_RHO_R1=<r1>; see
+  // ThetaArgs::r1): r1 in {2, 4}, n_rho divisible by r1, single plans of long
+  // columns only (the cluster split and slabs keep whole columns).
+  {
+    int r1 = 1;
+    if (const char* env = std::getenv("NWB_RHO_R1")) r1 = std::atoi(env);
+    if (r1 != 2 && r1 != 4) r1 = 1;
+    if (n_rho % r1 || n_rho / r1 < 8 || p->rho_split) r1 = 1;
+    // the theta CTAs hold r1 whole rows
+    if ((size_t)r1 * (n_theta / 2 + 64) * 2 * (precision == NWB_F64 ? 8 : 4) > 200 * 1024) r1 = 1;
+    p->rho_r1 = r1;
+    p->msub = n_rho / r1;
+  }
   int mp_r = 16, mp_h = 16;
   if (const char* env = std::getenv("NWB_MAXPROD_R")) mp_r = std::atoi(env);
   if (const char* env = std::getenv("NWB_MAXPROD_H")) mp_h = std::atoi(env);
-  if (!plan_fft(n_rho, p->rho_split != 0, p->plan_r, mp_r) || !plan_fft(p->g.m, false, p->plan_h, mp_h)) {
+  if (!plan_fft(n_rho, p->rho_split ? 2 : p->rho_r1, p->plan_r, mp_r) || !plan_fft(p->g.m, 0, p->plan_h, mp_h)) {
     delete p;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
   }
@@ -1443,6 +1526,10 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   int th = ((n_rho / 10) + 31) / 32 * 32;
   p->rho_threads = th < 128 ? 128 : (th > 512 ? 512 : th);  // small grids: latency-bound, keep 4 warps
   if (p->rho_split) p->rho_threads = p->rho_threads > 256 ? 256 : p->rho_threads;
+  if (p->rho_r1 > 1) {  // sub-columns: about one radix-10 butterfly per thread, <= 256
+    const int ts = ((p->msub / 10) + 31) / 32 * 32;
+    p->rho_threads = ts < 128 ? 128 : (ts > 256 ? 256 : ts);
+  }
   if (const char* env = std::getenv("NWB_RHO_THREADS")) {
     const int t = std::atoi(env);
     if (t >= 32 && t <= (p->rho_split ? 256 : 1024) && t % 32 == 0) p->rho_threads = t;
@@ -1480,6 +1567,7 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   p->overlap_chunks = 0;
   if (const char* env = std::getenv("NWB_OVERLAP")) p->overlap_chunks = std::atoi(env);
   if (p->overlap_chunks > 8) p->overlap_chunks = 8;
+  if (p->rho_r1 > 1) p->overlap_chunks = 0;  // r2c row chunks need whole-row CTAs
   if (p->overlap_chunks > 1) {
     e = cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking);
     for (int i = 0; i < 9 && e == cudaSuccess; ++i)

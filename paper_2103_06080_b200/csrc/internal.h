@@ -18,6 +18,7 @@ enum RhoMode {
   RHO_FWD_NAT = 4,  // out = F(bt) in natural order (no inverse)
   RHO_INV_NAT = 5,  // out = F^-1(in), `in` in natural order (vh = in, digit-reversed, if set)
   RHO_REV2NAT = 6,  // out = in permuted from digit-reversed to natural order
+  RHO_FWD_DR = 7,   // sub-columns: out = F(bt) in digit-reversed positions (then REV2NAT)
 };
 
 // Geometry of one plan: physical fields are (batch, nr, nt) real, spectral
@@ -52,6 +53,12 @@ template <typename T> struct ThetaArgs {
   // r2c row chunk [row_begin, row_end) (row_end 0 = all rows): the march overlaps
   // the r2c of one chunk with the WENO of the next on a side stream
   int row_begin, row_end;
+  // fused first rho stage (r1 > 1, SPLIT kernels): a CTA owns the rho rows
+  // i + r msub (r < r1, msub = nr / r1); r2c ends with the radix-r1 DIF stage of
+  // the rho FFT across them (y_q = sum_r X_r w^{rq} W_nr^{q i} -> position
+  // q msub + i), c2r starts with the matching DIT stage.  tw_first = W_nr^t, t < nr.
+  int r1, msub;
+  const cplx<T>* tw_first;
 };
 
 template <typename T> struct RhoArgs {
@@ -89,6 +96,15 @@ template <typename T> struct RhoArgs {
   int ws_ctas;
   int ws_debug;               // measurement: 1 = combine group idle, 2 = transform group skips FFTs
   cplx<T>* scratch;
+  // sub-column pass (k_rho_sub, r1 > 1): CTA (member, k r1 + q1) transforms the
+  // msub-point sub-column q1 (positions q1 msub + p'); dsub / tw_sub describe
+  // the msub-point transform (the full plan without its first stage); dr keeps
+  // the full transform for the j-symmetric table positions; rev_r = position
+  // -> frequency (natural-order gathers)
+  int r1;
+  FftDesc dsub;
+  const cplx<T>* tw_sub;
+  const int* rev_r;
 };
 
 template <typename T> struct WenoArgs {

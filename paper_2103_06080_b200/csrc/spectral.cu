@@ -59,8 +59,12 @@ template <int R> constexpr int theta_threads() { return R == 1 ? 128 : 256; }
 #ifndef NWB_THETA_MINB_R1
 #define NWB_THETA_MINB_R1 5
 #endif
-template <typename T, int R> constexpr int theta_min_blocks() {
-  return R == 1 ? (sizeof(T) == 8 ? NWB_THETA_MINB_R1 : 6) : (sizeof(T) == 8 ? NWB_THETA_MINB64 : 3);
+#ifndef NWB_THETA_MINB_SPLIT64
+#define NWB_THETA_MINB_SPLIT64 3
+#endif
+template <typename T, int R, bool SPLIT = false> constexpr int theta_min_blocks() {
+  return R == 1 ? (sizeof(T) == 8 ? NWB_THETA_MINB_R1 : 6)
+                : (sizeof(T) == 8 ? (SPLIT && R == 2 ? NWB_THETA_MINB_SPLIT64 : NWB_THETA_MINB64) : 3);
 }
 // an fp32 rho column (<= 113 KB) leaves room for a second CTA per SM, whose
 // loads then overlap this one's transforms
@@ -105,10 +109,10 @@ __device__ __forceinline__ void c2r_pre(cplx<T>* z, const ThetaArgs<T>& a, int r
   }
 }
 
-// scale, store R rows (j0 + r < nr) and fold their reductions into amax / vmax
+// scale, store R rows (j0 + r jstep < nr) and fold their reductions into amax / vmax
 template <typename T, int R>
 __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a, int rs, int mem,
-                                         int j0, int step, u64& amax, u64& vmax) {
+                                         int j0, int step, u64& amax, u64& vmax, int jstep = 1) {
   using V = cplx<T>;
   const int m = a.g.m, nr = a.g.nr;
   T* dst = a.phys_out + (size_t)mem * nr * a.g.nt;
@@ -117,7 +121,7 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
   const T scale = a.scale, bco = a.bcoef;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int j = j0 + r;
+    const int j = j0 + r * jstep;
     if (j >= nr) break;
     const V* zr = z + r * rs;
     V* drow = reinterpret_cast<V*>(dst + (size_t)j * a.g.nt);
@@ -143,31 +147,60 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
   }
 }
 
+// Fused last rho stage (SPLIT): slot r holds T'[k][r msub + i] (the r1
+// sub-column inverses); the radix-R DIT stage of the rho inverse,
+//   a_q = T'_q conj(W_nr^{q i}),  T[k][i + m msub] = sum_q a_q conj(w_R)^{mq},
+// turns them into the R physical rows i + m msub in place.
 template <typename T, int R>
-__global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())) k_theta_c2r(const ThetaArgs<T> a) {
+__device__ __forceinline__ void split_dit_rows(cplx<T>* z, const ThetaArgs<T>& a, int rs, int i) {
+  using V = cplx<T>;
+  V w[R];
+#pragma unroll
+  for (int q = 1; q < R; ++q) w[q] = __ldg(&a.tw_first[q * i]);
+  for (int k = threadIdx.x; k < a.g.kk; k += blockDim.x) {
+    const int sk = pidx(a.dh, k);
+    V v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = z[q * rs + sk];
+#pragma unroll
+    for (int q = 1; q < R; ++q) v[q] = cmulc(v[q], w[q]);
+    bfly<R, true>(v);
+#pragma unroll
+    for (int m = 0; m < R; ++m) z[m * rs + sk] = v[m];
+  }
+}
+
+// SPLIT: the CTA owns rows i + r msub (i = blockIdx.x < msub), else rows j0 + r
+template <typename T, int R, bool SPLIT>
+__global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R, SPLIT>())) k_theta_c2r(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
   const int kk = a.g.kk, nr = a.g.nr, ld = a.g.ld;
   const int rs = padded_len(a.g.m, a.dh.pad_period);  // smem row stride (holds X[0..m])
   const int mem = blockIdx.y;
-  const int j0 = blockIdx.x * R;
+  const int j0 = SPLIT ? (int)blockIdx.x : (int)blockIdx.x * R;
+  const int jstep = SPLIT ? a.msub : 1;
   const V* src = a.spec_in + (size_t)mem * kk * ld;
   for (int idx = threadIdx.x; idx < kk * R && !(a.debug & 4); idx += blockDim.x) {
-    const int r = idx % R, k = idx / R, j = j0 + r;
+    const int r = idx % R, k = idx / R, j = j0 + r * jstep;
     V* slot = &z[r * rs + pidx(a.dh, k)];
     if (j < nr) cp_async_c(slot, &src[(size_t)k * ld + j]);
     else *slot = mk<V>(0, 0);
   }
   cp_async_wait_all();
   __syncthreads();
+  if (SPLIT) {
+    split_dit_rows<T, R>(z, a, rs, j0);
+    __syncthreads();
+  }
   c2r_pre<T, R>(z, a, rs);
   __syncthreads();
   fft_inverse_dif(z, a.dh, R, rs, a.tw_h);
   if (a.debug & 4) return;
   const int step = a.step_ctr ? *a.step_ctr : 0;
   u64 amax = 0, vmax = 0;
-  c2r_post<T, R>(z, a, rs, mem, j0, step, amax, vmax);
+  c2r_post<T, R>(z, a, rs, mem, j0, step, amax, vmax, jstep);
   if (a.alpha_bits || a.vmax_bits) {
     block_max2<T>(amax, vmax,
                   a.alpha_bits ? a.alpha_bits + (size_t)mem * a.alpha_stride : nullptr,
@@ -206,20 +239,65 @@ __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a
   }
 }
 
+// Fused first rho stage (SPLIT): for each theta mode k the R rows' spectra
+// X_r[k] (rows i + r msub) go through the radix-R DIF stage of the rho FFT,
+//   y_q = (sum_r X_r w_R^{rq}) W_nr^{q i}  -> position q msub + i of column k.
 template <typename T, int R>
-__global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())) k_theta_r2c(const ThetaArgs<T> a) {
+__device__ __forceinline__ void r2c_post_split(const cplx<T>* z, const ThetaArgs<T>& a, int rs,
+                                               int mem, int i) {
+  using V = cplx<T>;
+  const int m = a.g.m, ld = a.g.ld, ms = a.msub;
+  V* dst = a.spec_out + (size_t)mem * a.g.kk * ld + i;
+  const int npairs = m / 2 + 1;
+  const T half = (T)0.5;
+  V w[R];
+#pragma unroll
+  for (int q = 1; q < R; ++q) w[q] = __ldg(&a.tw_first[q * i]);
+  for (int k = threadIdx.x; k < npairs; k += blockDim.x) {
+    const int pk = pidx(a.dh, __ldg(&a.pos_h[k]));
+    const int pm = pidx(a.dh, __ldg(&a.pos_h[k == 0 ? 0 : m - k]));
+    const V wk = __ldg(&a.wk[k]);
+    V xk[R], xm[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const V zk = z[r * rs + pk], zm = z[r * rs + pm];
+      const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
+      const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
+      const V wz = cmul(wk, zo);
+      xk[r] = cadd(ze, wz);
+      const V d = csub(ze, wz);
+      xm[r] = mk<V>(d.x, -d.y);
+    }
+    bfly<R, false>(xk);
+#pragma unroll
+    for (int q = 1; q < R; ++q) xk[q] = cmul(xk[q], w[q]);
+#pragma unroll
+    for (int q = 0; q < R; ++q) dst[(size_t)k * ld + q * ms] = xk[q];
+    if (2 * k != m) {
+      bfly<R, false>(xm);
+#pragma unroll
+      for (int q = 1; q < R; ++q) xm[q] = cmul(xm[q], w[q]);
+#pragma unroll
+      for (int q = 0; q < R; ++q) dst[(size_t)(m - k) * ld + q * ms] = xm[q];
+    }
+  }
+}
+
+template <typename T, int R, bool SPLIT>
+__global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R, SPLIT>())) k_theta_r2c(const ThetaArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
   const int m = a.g.m, nr = a.g.nr;
-  const int jend = a.row_end ? a.row_end : nr;
+  const int jend = SPLIT ? nr : (a.row_end ? a.row_end : nr);
   const int mem = blockIdx.y;
-  const int j0 = a.row_begin + blockIdx.x * R;
+  const int j0 = SPLIT ? (int)blockIdx.x : a.row_begin + (int)blockIdx.x * R;
+  const int jstep = SPLIT ? a.msub : 1;
   const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
   const int rs = padded_len(m, a.dh.pad_period);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int j = j0 + r;
+    const int j = j0 + r * jstep;
     V* zr = z + r * rs;
     const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
     for (int n = threadIdx.x; n < m && !(a.debug & 4); n += blockDim.x) {
@@ -231,7 +309,8 @@ __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R>())
   __syncthreads();
   fft_forward(z, a.dh, R, rs, a.tw_h);
   if (a.debug & 4) return;
-  r2c_post<T, R>(z, a, rs, mem, j0);
+  if (SPLIT) r2c_post_split<T, R>(z, a, rs, mem, j0);
+  else r2c_post<T, R>(z, a, rs, mem, j0);
 }
 
 // ------------------------------------------------------------------ theta passes, streaming
@@ -358,7 +437,8 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
                                             const cplx<T>* __restrict__ P2,
                                             cplx<T>* __restrict__ vh, cplx<T>* __restrict__ u,
                                             T ds, int debug, int tid = threadIdx.x,
-                                            int nth = blockDim.x, int roll = 0) {
+                                            int nth = blockDim.x, int roll = 0,
+                                            const FftDesc* dsym = nullptr, int pofs = 0) {
   using V = cplx<T>;
   constexpr int U = 4;
   const bool nl = debug & 2;
@@ -387,7 +467,8 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
       if (p < n) {
         sp[q] = XG ? p : pidx(d, p);
         b[q] = x[sp[q]];
-        const int tp = sym_pos(d, p);  // tables: canonical +-f position
+        // tables: canonical +-f position (sub-columns: of global position pofs + p)
+        const int tp = dsym ? sym_pos(*dsym, pofs + p) : sym_pos(d, p);
         if (MODE == RHO_STAGE1 && !nl) {
           o1[q] = E[tp]; o2[q] = vh[p]; o3[q] = P1[tp]; o4[q] = P12[tp];
         } else if (MODE == RHO_STAGE2) {
@@ -488,6 +569,64 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   if (!(a.debug & 4))
     for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+}
+
+// ------------------------------------------------------------------ rho pass, sub-columns
+// With the first rho stage fused into the theta passes (ThetaArgs::r1), a rho
+// column k splits into r1 independent msub-point sub-columns: position
+// q1 msub + p' of the digit-reversed spectrum is position p' of the msub-point
+// DIF transform of sub-column q1 (the r1-radix stage is the transform's
+// first).  One CTA per sub-column: a C2 fp64 column (160 KB) becomes two
+// 80 KB sub-columns, so two CTAs share an SM and one streams while the other
+// transforms.  Modes as k_rho; RHO_FWD_DR stores the forward transform in
+// digit-reversed positions (rfft2 then permutes with RHO_REV2NAT) and
+// RHO_INV_NAT gathers its natural-order input by position -> frequency.
+#ifndef NWB_RHO_SUB_MINB64
+#define NWB_RHO_SUB_MINB64 2
+#endif
+template <typename T> constexpr int rho_sub_min_blocks() { return sizeof(T) == 8 ? NWB_RHO_SUB_MINB64 : 3; }
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256, rho_sub_min_blocks<T>()) k_rho_sub(const RhoArgs<T> a) {
+  using V = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* x = reinterpret_cast<V*>(smem_raw);
+  const FftDesc& d = a.dsub;
+  const int ms = d.n, r1 = a.r1;
+  const int mem = blockIdx.x, k = blockIdx.y / r1, q1 = blockIdx.y - k * r1;
+  const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+  const size_t sub = row + (size_t)q1 * ms;
+  const size_t trow = (size_t)k * a.g.ld;
+  if (MODE == RHO_INV_NAT) {
+    // natural-order column in: gather this sub-column's positions
+    const int* fr = a.rev_r + (size_t)q1 * ms;
+    for (int p = threadIdx.x; p < ms; p += blockDim.x) {
+      const V val = a.in[row + __ldg(&fr[p])];
+      x[pidx(d, p)] = val;
+      if (a.vh) a.vh[sub + p] = val;
+    }
+  } else {
+    const V* src = a.in + sub;
+    for (int j = threadIdx.x; j < ms; j += blockDim.x) cp_async_c(&x[pidx(d, j)], &src[j]);
+    cp_async_wait_all();
+  }
+  if (a.zero_bits && blockIdx.y == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
+  __syncthreads();
+  if (MODE != RHO_INV_NAT) fft_forward(x, d, 1, 0, a.tw_sub);
+  if (MODE == RHO_FWD_DR) {
+    V* dst = a.out + sub;
+    for (int p = threadIdx.x; p < ms; p += blockDim.x) dst[p] = x[pidx(d, p)];
+    return;
+  }
+  if (MODE != RHO_INV_NAT)
+    rho_combine<T, MODE>(x, d, ms, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
+                         a.vh + sub, a.u + sub, a.ds, 0, threadIdx.x, blockDim.x, 0, &a.dr,
+                         q1 * ms);
+  __syncthreads();
+  fft_inverse(x, d, 1, 0, a.tw_sub);
+  V* dst = a.out + sub;
+  for (int j = threadIdx.x; j < ms; j += blockDim.x) dst[j] = x[pidx(d, j)];
+  if (a.step_ctr && mem == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.step_ctr += 1;
 }
 
 // ------------------------------------------------------------------ rho pass, warp-specialised
@@ -797,20 +936,20 @@ template <int R> static int theta_block(int m) {
   return R > 1 && R * m <= 2048 ? 128 : theta_threads<R>();
 }
 
-template <typename T, int R>
+template <typename T, int R, bool SPLIT = false>
 static void c2r_r(const ThetaArgs<T>& a, cudaStream_t s) {
   const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
-  cudaFuncSetAttribute(k_theta_c2r<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid((a.g.nr + R - 1) / R, a.g.batch);
-  k_theta_c2r<T, R><<<grid, theta_block<R>(a.g.m), sm, s>>>(a);
+  cudaFuncSetAttribute(k_theta_c2r<T, R, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  dim3 grid(SPLIT ? a.msub : (a.g.nr + R - 1) / R, a.g.batch);
+  k_theta_c2r<T, R, SPLIT><<<grid, theta_block<R>(a.g.m), sm, s>>>(a);
 }
-template <typename T, int R>
+template <typename T, int R, bool SPLIT = false>
 static void r2c_r(const ThetaArgs<T>& a, cudaStream_t s) {
   const size_t sm = (size_t)R * padded_len(a.g.m, a.dh.pad_period) * sizeof(cplx<T>);
-  cudaFuncSetAttribute(k_theta_r2c<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_theta_r2c<T, R, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int nrows = (a.row_end ? a.row_end : a.g.nr) - a.row_begin;
-  dim3 grid((nrows + R - 1) / R, a.g.batch);
-  k_theta_r2c<T, R><<<grid, theta_block<R>(a.g.m), sm, s>>>(a);
+  dim3 grid(SPLIT ? a.msub : (nrows + R - 1) / R, a.g.batch);
+  k_theta_r2c<T, R, SPLIT><<<grid, theta_block<R>(a.g.m), sm, s>>>(a);
 }
 
 static int sm_count() {
@@ -834,8 +973,14 @@ static void theta_stream(const ThetaArgs<T>& a, cudaStream_t s) {
   kern<<<ctas, 512, sm, s>>>(a);
 }
 
-// rows < 0 selects the persistent double-buffered kernel with R = -rows
+// rows < 0 selects the persistent double-buffered kernel with R = -rows;
+// a.r1 > 1 the fused-rho-stage kernels with R = r1 rows at stride msub
 template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s) {
+  if (a.r1 > 1) {
+    if (a.r1 == 4) c2r_r<T, 4, true>(a, s);
+    else c2r_r<T, 2, true>(a, s);
+    return;
+  }
   switch (rows) {
     case -1: theta_stream<T, 1, true>(a, s); break;
     case -2: theta_stream<T, 2, true>(a, s); break;
@@ -848,6 +993,11 @@ template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cud
   }
 }
 template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cudaStream_t s) {
+  if (a.r1 > 1) {
+    if (a.r1 == 4) r2c_r<T, 4, true>(a, s);
+    else r2c_r<T, 2, true>(a, s);
+    return;
+  }
   switch (rows) {
     case -1: theta_stream<T, 1, false>(a, s); break;
     case -2: theta_stream<T, 2, false>(a, s); break;
@@ -862,6 +1012,18 @@ template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cud
 
 template <typename T, int MODE>
 static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
+  if constexpr (MODE != RHO_REV2NAT && MODE != RHO_FWD_NAT) {
+    if (a.r1 > 1) {
+      const size_t sm = (size_t)padded_len(a.dsub.n, a.dsub.pad_period) * sizeof(cplx<T>);
+      cudaFuncSetAttribute(k_rho_sub<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      dim3 grid(a.g.batch, a.g.kk * a.r1);
+      k_rho_sub<T, MODE><<<grid, threads > 256 ? 256 : threads, sm, s>>>(a);
+      return;
+    }
+  }
+  if constexpr (MODE == RHO_FWD_DR) {
+    return;  // sub-column mode only
+  } else {
   if constexpr (MODE <= RHO_INIT) {
     if (a.split) {
       const size_t sm = (size_t)padded_len(a.dh2.n, a.dh2.pad_period) * sizeof(cplx<T>);
@@ -897,6 +1059,7 @@ static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
   cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid(a.g.batch, a.g.kk);
   k_rho<T, MODE><<<grid, threads, sm, s>>>(a);
+  }
 }
 
 template <typename T> void launch_rho(const RhoArgs<T>& a, int mode, int threads, cudaStream_t s) {
@@ -907,6 +1070,7 @@ template <typename T> void launch_rho(const RhoArgs<T>& a, int mode, int threads
     case RHO_INIT: rho_m<T, RHO_INIT>(a, threads, s); break;
     case RHO_FWD_NAT: rho_m<T, RHO_FWD_NAT>(a, threads, s); break;
     case RHO_INV_NAT: rho_m<T, RHO_INV_NAT>(a, threads, s); break;
+    case RHO_FWD_DR: rho_m<T, RHO_FWD_DR>(a, threads, s); break;
     default: rho_m<T, RHO_REV2NAT>(a, threads, s); break;
   }
 }
