@@ -201,6 +201,38 @@ int nwb_combine(int precision, long long n, int mode, double d_sigma, const void
                 const void* vh_dev, const void* b1_dev, const void* b2_dev, void* out_dev,
                 void* stream);
 
+/*
+ * Splitting baseline -> run_splitting / lie_step and the
+ * stage functions of splitting.py:78-301.  Float64 only (the reference has
+ * no precision switch).  Fields are (n_nodes, n_theta) row-major on the
+ * closed rho grid (n_nodes = N_rho + 1); coefficient rows (n_rows, ld) cover
+ * at least n_nodes entries each.
+ *   nwb_split_stage: 0 step_diffraction_cn (splitting.py:138-145),
+ *     1 step_burgers_godunov (:169-177), 2 step_axial_absorption_spectral
+ *     (:180-201, coefficient row sigma_row), 3 step_transverse_lw (:204-223),
+ *     4 lie_step (:233-250).
+ *   nwb_split_march: n_steps Lie steps of the loaded state from step n0 with
+ *     the divergence guard (max|V| per step to max_abs, host), the budget
+ *     (max_seconds < 0: none) -- run_splitting :253-301.
+ *   nwb_godunov_flux -> godunov_flux (:157-166) on device arrays.
+ */
+typedef struct nwb_split nwb_split;
+int nwb_split_create(nwb_split** plan, int n_nodes, int n_theta, double d_sigma, double d_rho,
+                     double d_theta, double theta_span, double A, double B, int device);
+int nwb_split_destroy(nwb_split* plan);
+int nwb_split_set_stream(nwb_split* plan, void* stream);
+int nwb_split_set_coeffs(nwb_split* plan, const double* u_par, const double* u_perp,
+                         const double* du_perp_dsigma, const double* du_perp_drho, int n_rows,
+                         int ld, int on_device);
+int nwb_split_load(nwb_split* plan, const double* v_dev);
+int nwb_split_store(nwb_split* plan, double* v_dev);
+int nwb_split_stage(nwb_split* plan, int stage, int sigma_row, const double* in_dev,
+                    double* out_dev);
+int nwb_split_march(nwb_split* plan, int n0, int n_steps, double guard, double max_seconds,
+                    double* max_abs, int* fail_step, double* fail_value);
+int nwb_godunov_flux(long long n, const double* u_l_dev, const double* u_r_dev, double B,
+                     double* out_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,9 @@ from .analysis import (GRID_SETS, GroundMetrics, ensemble_nwaves, ground_metrics
 from .studies import (CheckpointComparison, ComparisonReport, ConvergenceRow, ScalingRow,
                       TimingReport, compare_solvers, convergence_rate, convergence_study,
                       cost_scaling_study, max_overshoot)
+from .splitting import (SplittingState, godunov_flux, lie_step, run_splitting,
+                        step_axial_absorption_spectral, step_burgers_godunov,
+                        step_diffraction_cn, step_transverse_lw)
 from . import fieldio
 
 __all__ = [
@@ -45,4 +48,7 @@ __all__ = [
     "initial_nwave", "preset_config", "rho_modulated", "CheckpointComparison",
     "ComparisonReport", "ConvergenceRow", "ScalingRow", "TimingReport", "compare_solvers",
     "convergence_rate", "convergence_study", "cost_scaling_study", "max_overshoot", "fieldio",
+    "SplittingState", "godunov_flux", "lie_step", "run_splitting",
+    "step_axial_absorption_spectral", "step_burgers_godunov", "step_diffraction_cn",
+    "step_transverse_lw",
 ]

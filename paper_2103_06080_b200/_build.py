@@ -34,6 +34,7 @@ UNITS = [
     ("weno", "weno.cu", []),
     ("capi", "capi.cu", []),
     ("tables", "tables.cu", ["-fmad=false"]),
+    ("splitting", "splitting.cu", ["-fmad=false"]),
     ("metrics", "metrics.cu", []),
 ]
 

@@ -37,7 +37,9 @@ ABI_SYMBOLS = (
     "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine", "nwb_profile_kernels",
     "nwb_turbulence_fields", "nwb_slab_create", "nwb_slab_destroy", "nwb_slab_set_stream",
     "nwb_slab_layout", "nwb_slab_set_coeffs", "nwb_slab_theta_c2r", "nwb_slab_weno",
-    "nwb_slab_theta_r2c", "nwb_slab_rho", "nwb_ground_metrics",
+    "nwb_slab_theta_r2c", "nwb_slab_rho", "nwb_ground_metrics", "nwb_split_create",
+    "nwb_split_destroy", "nwb_split_set_stream", "nwb_split_set_coeffs", "nwb_split_load",
+    "nwb_split_store", "nwb_split_stage", "nwb_split_march", "nwb_godunov_flux",
 )
 
 _lock = threading.Lock()
@@ -97,6 +99,18 @@ def _declare(lib):
                                           c_void_p, c_void_p, c_void_p]),
         "nwb_combine": (c_int, [c_int, c_ll, c_int, c_double, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+        "nwb_split_create": (c_int, [P(c_void_p), c_int, c_int, c_double, c_double, c_double,
+                                     c_double, c_double, c_double, c_int]),
+        "nwb_split_destroy": (c_int, [c_void_p]),
+        "nwb_split_set_stream": (c_int, [c_void_p, c_void_p]),
+        "nwb_split_set_coeffs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                         c_int, c_int]),
+        "nwb_split_load": (c_int, [c_void_p, c_void_p]),
+        "nwb_split_store": (c_int, [c_void_p, c_void_p]),
+        "nwb_split_stage": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p]),
+        "nwb_split_march": (c_int, [c_void_p, c_int, c_int, c_double, c_double, c_void_p,
+                                    P(c_int), P(c_double)]),
+        "nwb_godunov_flux": (c_int, [c_ll, c_void_p, c_void_p, c_double, c_void_p, c_void_p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

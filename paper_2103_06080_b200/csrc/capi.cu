@@ -287,7 +287,7 @@ struct nwb_plan {
   void* ws_scratch = nullptr;
   // first rho stage fused into the theta passes (r1 > 1): rho CTAs own
   // msub = nr / r1 point sub-columns (dsub / tw_sub); tw_first = W_nr^t
-  int rho_r1 = 1, msub = 0;
+  int rho_r1 = 1, msub = 0, ilv = 1;
   FftDesc dsub{};
   void *tw_sub = nullptr, *tw_first = nullptr;
   FftDesc dh2{};             // half-column descriptor (split mode)
@@ -385,6 +385,7 @@ template <typename T> ThetaArgs<T> theta_args(const nwb_plan* p) {
   a.r1 = p->rho_r1;
   a.msub = p->msub;
   a.tw_first = (const cplx<T>*)p->tw_first;
+  a.ilv = p->ilv;
   return a;
 }
 
@@ -417,6 +418,7 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.tw_h2 = (const cplx<T>*)p->tw_h2;
   a.tw_split = (const cplx<T>*)p->tw_split;
   a.r1 = p->rho_r1;
+  a.ilv = p->ilv;
   a.dsub = p->dsub;
   a.tw_sub = (const cplx<T>*)p->tw_sub;
   a.rev_r = p->rev_r;
@@ -1296,6 +1298,197 @@ template <typename T> int slab_rho_impl(nwb_slab* s, int mode, const void* bt, v
 
 }  // namespace
 
+// ====================================================================== splitting baseline
+// SURVEY row f4 (reference splitting.py): the Lie-Trotter solver on the closed
+// rho grid, float64.  Kernels in csrc/splitting.cu; the theta transforms of
+// the axial/absorption stage are the march's theta kernels on a rho extent of
+// n = N_rho + 1 rows.
+
+struct nwb_split {
+  int device = 0;
+  cudaStream_t stream = 0, own_stream = 0;
+  int n = 0, nt = 0, ldn = 0;
+  Geom g{};
+  double d_sigma = 0, d_rho = 0, d_theta = 0, theta_span = 0, A = 0, B = 0, gamma = 0;
+  FftDesc dh{};
+  FftPlanHost plan_h;
+  int theta_rows = 1;
+  void *tw_h = nullptr, *wk = nullptr;
+  int* pos_h = nullptr;
+  double *w = nullptr, *upper = nullptr, *diag = nullptr;   // Thomas factorisation
+  double *v = nullptr, *t1 = nullptr, *t2 = nullptr, *vT = nullptr, *sT = nullptr;
+  double* gline = nullptr;  // diffraction rho lines when they exceed shared memory
+  void* spec = nullptr;
+  double *upar = nullptr, *uperp = nullptr, *dus = nullptr, *dur = nullptr;
+  int n_rows = 0;
+  u64* hist = nullptr;
+  int hist_len = 0;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int xalloc(nwb_split* s, void** ptr, size_t bytes) {
+  cudaError_t e = cudaMallocAsync(ptr, bytes ? bytes : 16, s->stream);
+  if (e != cudaSuccess) {
+    *ptr = nullptr;
+    return fail(e == cudaErrorMemoryAllocation ? NWB_ENOMEM : NWB_ECUDA,
+                std::string("split alloc: ") + cudaGetErrorString(e));
+  }
+  s->allocs.push_back(*ptr);
+  return NWB_OK;
+}
+
+int split_create_impl(nwb_split* s) {
+  const size_t C = sizeof(double2);
+  std::vector<double2> twh;
+  build_desc<double>(s->g.m, s->plan_h, s->dh, twh);
+  auto wk = twiddles<double>(s->nt, s->g.kk);
+  auto fh = freq_of_pos(s->g.m, s->plan_h.stages);
+  std::vector<int> ph(s->g.m);
+  for (int q = 0; q < s->g.m; ++q) ph[fh[q]] = q;
+  // Thomas factorisation exactly as the reference builds it (splitting.py:103-113)
+  const int n = s->n;
+  const double c = 0.5 * s->gamma;
+  std::vector<double> lower(n, -c), upper(n, -c), diag(n), w(n, 0.0);
+  lower[n - 1] = -2.0 * c;
+  upper[0] = -2.0 * c;
+  diag[0] = 1.0 + 2.0 * c;
+  for (int j = 1; j < n; ++j) {
+    w[j] = lower[j] / diag[j - 1];
+    diag[j] = (1.0 + 2.0 * c) - w[j] * upper[j - 1];
+  }
+  TRY(xalloc(s, &s->tw_h, twh.size() * C));
+  TRY(xalloc(s, &s->wk, wk.size() * C));
+  TRY(xalloc(s, (void**)&s->pos_h, ph.size() * sizeof(int)));
+  TRY(xalloc(s, (void**)&s->w, n * sizeof(double)));
+  TRY(xalloc(s, (void**)&s->upper, n * sizeof(double)));
+  TRY(xalloc(s, (void**)&s->diag, n * sizeof(double)));
+  const size_t phys = (size_t)n * s->nt * sizeof(double);
+  for (double** b : {&s->v, &s->t1, &s->t2}) TRY(xalloc(s, (void**)b, phys));
+  TRY(xalloc(s, (void**)&s->vT, (size_t)s->nt * s->ldn * sizeof(double)));
+  TRY(xalloc(s, (void**)&s->sT, (size_t)s->nt * s->ldn * sizeof(double)));
+  TRY(xalloc(s, &s->spec, (size_t)s->g.kk * s->g.ld * C));
+  if (!split_line_in_smem(n)) TRY(xalloc(s, (void**)&s->gline, (size_t)3 * n * sizeof(double)));
+  CU(cudaMemsetAsync(s->spec, 0, (size_t)s->g.kk * s->g.ld * C, s->stream));
+  CU(cudaMemcpyAsync(s->tw_h, twh.data(), twh.size() * C, cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->wk, wk.data(), wk.size() * C, cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->pos_h, ph.data(), ph.size() * sizeof(int), cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->w, w.data(), n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->upper, upper.data(), n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  CU(cudaMemcpyAsync(s->diag, diag.data(), n * sizeof(double), cudaMemcpyHostToDevice, s->stream));
+  CU(cudaStreamSynchronize(s->stream));
+  return NWB_OK;
+}
+
+ThetaArgs<double> split_theta_args(const nwb_split* s) {
+  ThetaArgs<double> a{};
+  a.g = s->g;
+  a.dh = s->dh;
+  a.tw_h = (const double2*)s->tw_h;
+  a.wk = (const double2*)s->wk;
+  a.pos_h = s->pos_h;
+  a.scale = 1.0 / (double)s->nt;  // a 1-D theta inverse (scipy irfft along axis 1)
+  a.r1 = 1;
+  return a;
+}
+
+// stage: 0 diffraction, 1 Burgers, 2 axial + absorption (coefficient row `row`),
+// 3 transverse (row `row`), 4 the whole Lie step; vmax (device) gets max|out|
+// of the transverse stage
+int split_stage(nwb_split* s, int stage, int row, const double* in, double* out, u64* vmax) {
+  const int n = s->n, nt = s->nt;
+  cudaStream_t st = s->stream;
+  if ((stage == 2 || stage == 3 || stage == 4) && (row < 0 || row >= s->n_rows))
+    return fail(NWB_EINVAL, "splitting: coefficient row out of range (nwb_split_set_coeffs)");
+  const double* cur = in;
+  auto dst = [&](int last) -> double* { return stage == 4 ? (last ? out : (cur == s->t1 ? s->t2 : s->t1)) : out; };
+  if (stage == 0 || stage == 4) {
+    launch_split_prep(cur, n, nt, s->ldn, s->vT, s->sT, st);
+    double* o = dst(0);
+    launch_split_diffraction(s->vT, s->sT, n, nt, s->ldn, s->gamma, s->w, s->upper, s->diag, o,
+                             s->gline, st);
+    cur = o;
+  }
+  if (stage == 1 || stage == 4) {
+    double* o = dst(0);
+    launch_split_burgers(cur, n, nt, s->B, s->d_sigma / s->d_theta, o, st);
+    cur = o;
+  }
+  if (stage == 2 || stage == 4) {
+    ThetaArgs<double> r = split_theta_args(s);
+    r.phys_in = cur;
+    r.spec_out = (double2*)s->spec;
+    launch_theta_r2c<double>(r, s->theta_rows, st);
+    launch_split_axial((double2*)s->spec, n, s->g.kk, s->g.ld, s->upar + (size_t)row * n,
+                       s->d_sigma, s->A, s->theta_span, st);
+    double* o = dst(0);
+    ThetaArgs<double> c = split_theta_args(s);
+    c.spec_in = (const double2*)s->spec;
+    c.phys_out = o;
+    launch_theta_c2r<double>(c, s->theta_rows, st);
+    cur = o;
+  }
+  if (stage == 3 || stage == 4) {
+    launch_split_transverse(cur, n, nt, s->uperp + (size_t)row * n, s->dus + (size_t)row * n,
+                            s->dur + (size_t)row * n, s->d_sigma, s->d_rho, out, vmax, st);
+  }
+  CHECK_LAUNCH("splitting stage");
+  return NWB_OK;
+}
+
+int split_march_impl(nwb_split* s, int n0, int n_steps, double guard, double max_seconds,
+                     double* max_abs, int* fail_step, double* fail_value) {
+  if (n_steps <= 0) return NWB_OK;
+  if (n0 < 0 || n0 + n_steps > s->n_rows)
+    return fail(NWB_EINVAL, "splitting: coefficient rows do not cover the march");
+  if (s->hist_len < n_steps) {
+    if (s->hist) cudaFreeAsync(s->hist, s->stream);
+    s->hist = nullptr;
+    CU(cudaMallocAsync((void**)&s->hist, (size_t)n_steps * sizeof(u64), s->stream));
+    s->hist_len = n_steps;
+  }
+  CU(cudaMemsetAsync(s->hist, 0, (size_t)n_steps * sizeof(u64), s->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  const bool budget = max_seconds >= 0;
+  std::vector<u64> h;
+  int done = 0;
+  while (done < n_steps) {
+    const int cnt = std::min(budget ? (done == 0 ? 1 : 8) : 32, n_steps - done);
+    for (int i = 0; i < cnt; ++i) {
+      // the step's output lands back in s->v (Lie step: v -> t1/t2 chain -> v)
+      TRY(split_stage(s, 4, n0 + done + i, s->v, s->v, s->hist + done + i));
+    }
+    h.resize(cnt);
+    CU(cudaMemcpyAsync(h.data(), s->hist + done, cnt * sizeof(u64), cudaMemcpyDeviceToHost, s->stream));
+    CU(cudaStreamSynchronize(s->stream));
+    for (int i = 0; i < cnt; ++i) {
+      double m;
+      std::memcpy(&m, &h[i], sizeof(double));
+      if (max_abs) max_abs[done + i] = m;
+      if (!(std::isfinite(m) && m <= guard)) {
+        if (fail_step) *fail_step = n0 + done + i;
+        if (fail_value) *fail_value = m;
+        char msg[160];
+        std::snprintf(msg, sizeof msg, "max|V| left the guard: step=%d member=0 max_abs=%.17g",
+                      n0 + done + i, m);
+        return fail(NWB_EINSTABILITY, msg);
+      }
+    }
+    done += cnt;
+    if (budget) {
+      const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > max_seconds) {
+        if (fail_step) *fail_step = n0 + done;
+        return fail(NWB_EBUDGET, "wall-clock budget exhausted");
+      }
+    }
+  }
+  return NWB_OK;
+}
+
+}  // namespace
+
 // ====================================================================== C ABI
 
 int nwb_slab_create(nwb_slab** out, int n_rho, int n_theta, int j0, int rows, int k0, int modes,
@@ -1483,6 +1676,7 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     if ((size_t)r1 * (n_theta / 2 + 64) * 2 * (precision == NWB_F64 ? 8 : 4) > 200 * 1024) r1 = 1;
     p->rho_r1 = r1;
     p->msub = n_rho / r1;
+    if (const char* env = std::getenv("NWB_RHO_ILV")) p->ilv = env[0] != '0';
   }
   int mp_r = 16, mp_h = 16;
   if (const char* env = std::getenv("NWB_MAXPROD_R")) mp_r = std::atoi(env);
@@ -1762,6 +1956,144 @@ int nwb_combine(int precision, long long n, int mode, double ds, const void* E, 
                           (const float2*)P2, (const float2*)vh, (const float2*)b1, (const float2*)b2,
                           (float2*)out, s);
   CHECK_LAUNCH("combine");
+  return NWB_OK;
+}
+
+
+int nwb_split_create(nwb_split** out, int n_nodes, int n_theta, double d_sigma, double d_rho,
+                     double d_theta, double theta_span, double A, double B, int device) {
+  if (!out) return fail(NWB_EINVAL, "null splitting plan pointer");
+  *out = nullptr;
+  if (n_nodes < 3 || n_theta < 2) return fail(NWB_EINVAL, "splitting: grid too small");
+  if (n_theta % 2) return fail(NWB_EUNSUPPORTED, "n_theta must be even (half-length real FFT)");
+  nwb_split* s = new nwb_split();
+  s->device = device;
+  s->n = n_nodes;
+  s->nt = n_theta;
+  s->ldn = (n_nodes + 31) / 32 * 32;
+  s->g.nr = n_nodes;
+  s->g.nt = n_theta;
+  s->g.m = n_theta / 2;
+  s->g.kk = n_theta / 2 + 1;
+  s->g.ld = (n_nodes + 7) / 8 * 8;
+  s->g.batch = 1;
+  s->d_sigma = d_sigma;
+  s->d_rho = d_rho;
+  s->d_theta = d_theta;
+  s->theta_span = theta_span;
+  s->A = A;
+  s->B = B;
+  s->gamma = d_sigma * d_theta / (8.0 * 3.141592653589793 * (d_rho * d_rho));
+  if (!plan_fft(s->g.m, 0, s->plan_h)) {
+    delete s;
+    return fail(NWB_EUNSUPPORTED, "n_theta/2 must factor into 2, 3, 5, 7");
+  }
+  const size_t row_bytes = (size_t)s->g.m * 16;
+  s->theta_rows = 1;
+  for (int r : {8, 4, 2})
+    if ((size_t)r * row_bytes <= 64 * 1024 && (n_nodes + r - 1) / r >= 2 * 148) {
+      s->theta_rows = r;
+      break;
+    }
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&s->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete s;
+    return fail(NWB_ECUDA, std::string("splitting device/stream: ") + cudaGetErrorString(e));
+  }
+  s->stream = s->own_stream;
+  keep_pool_memory(device);
+  int rc = split_create_impl(s);
+  if (rc != NWB_OK) {
+    nwb_split_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return NWB_OK;
+}
+
+int nwb_split_destroy(nwb_split* s) {
+  if (!s) return NWB_OK;
+  cudaSetDevice(s->device);
+  cudaStreamSynchronize(s->stream);
+  for (void* a : s->allocs)
+    if (a) cudaFreeAsync(a, s->stream);
+  if (s->hist) cudaFreeAsync(s->hist, s->stream);
+  for (double* a : {s->upar, s->uperp, s->dus, s->dur})
+    if (a) cudaFreeAsync(a, s->stream);
+  cudaStreamSynchronize(s->stream);
+  if (s->own_stream) cudaStreamDestroy(s->own_stream);
+  delete s;
+  return NWB_OK;
+}
+
+int nwb_split_set_stream(nwb_split* s, void* stream) {
+  if (!s) return fail(NWB_EINVAL, "null splitting plan");
+  s->stream = stream ? (cudaStream_t)stream : s->own_stream;
+  return NWB_OK;
+}
+
+int nwb_split_set_coeffs(nwb_split* s, const double* u_par, const double* u_perp,
+                         const double* du_dsigma, const double* du_drho, int n_rows, int ld,
+                         int on_device) {
+  if (!s) return fail(NWB_EINVAL, "null splitting plan");
+  if (n_rows < 1 || ld < s->n) return fail(NWB_EINVAL, "splitting: coefficient rows / ld too small");
+  CU(cudaSetDevice(s->device));
+  for (double** a : {&s->upar, &s->uperp, &s->dus, &s->dur}) {
+    if (*a) cudaFreeAsync(*a, s->stream);
+    *a = nullptr;
+  }
+  const double* src[4] = {u_par, u_perp, du_dsigma, du_drho};
+  double** dst[4] = {&s->upar, &s->uperp, &s->dus, &s->dur};
+  for (int i = 0; i < 4; ++i) {
+    CU(cudaMallocAsync((void**)dst[i], (size_t)n_rows * s->n * sizeof(double), s->stream));
+    if (!src[i]) {
+      CU(cudaMemsetAsync(*dst[i], 0, (size_t)n_rows * s->n * sizeof(double), s->stream));
+      continue;
+    }
+    CU(cudaMemcpy2DAsync(*dst[i], s->n * sizeof(double), src[i], (size_t)ld * sizeof(double),
+                         s->n * sizeof(double), n_rows,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s->stream));
+  }
+  s->n_rows = n_rows;
+  CU(cudaStreamSynchronize(s->stream));
+  return NWB_OK;
+}
+
+int nwb_split_load(nwb_split* s, const double* v) {
+  if (!s) return fail(NWB_EINVAL, "null splitting plan");
+  CU(cudaSetDevice(s->device));
+  CU(cudaMemcpyAsync(s->v, v, (size_t)s->n * s->nt * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+  return NWB_OK;
+}
+
+int nwb_split_store(nwb_split* s, double* v) {
+  if (!s) return fail(NWB_EINVAL, "null splitting plan");
+  CU(cudaSetDevice(s->device));
+  CU(cudaMemcpyAsync(v, s->v, (size_t)s->n * s->nt * sizeof(double), cudaMemcpyDeviceToDevice, s->stream));
+  return NWB_OK;
+}
+
+int nwb_split_stage(nwb_split* s, int stage, int sigma_row, const double* in, double* out) {
+  if (!s) return fail(NWB_EINVAL, "null splitting plan");
+  if (stage < 0 || stage > 4) return fail(NWB_EINVAL, "splitting: unknown stage");
+  if (in == out) return fail(NWB_EINVAL, "splitting: stage in and out must differ");
+  CU(cudaSetDevice(s->device));
+  return split_stage(s, stage, sigma_row, in, out, nullptr);
+}
+
+int nwb_split_march(nwb_split* s, int n0, int n_steps, double guard, double max_seconds,
+                    double* max_abs, int* fail_step, double* fail_value) {
+  if (!s) return fail(NWB_EINVAL, "null splitting plan");
+  CU(cudaSetDevice(s->device));
+  return split_march_impl(s, n0, n_steps, guard, max_seconds, max_abs, fail_step, fail_value);
+}
+
+int nwb_godunov_flux(long long n, const double* u_l, const double* u_r, double B, double* out,
+                     void* stream) {
+  if (n < 0) return fail(NWB_EINVAL, "negative length");
+  launch_godunov_flux((long)n, u_l, u_r, B, out, (cudaStream_t)stream);
+  CHECK_LAUNCH("godunov_flux");
   return NWB_OK;
 }
 

@@ -59,6 +59,7 @@ template <typename T> struct ThetaArgs {
   // q msub + i), c2r starts with the matching DIT stage.  tw_first = W_nr^t, t < nr.
   int r1, msub;
   const cplx<T>* tw_first;
+  int ilv;                    // transit layout: 1 = position q msub + i stored at i r1 + q
 };
 
 template <typename T> struct RhoArgs {
@@ -101,7 +102,7 @@ template <typename T> struct RhoArgs {
   // the msub-point transform (the full plan without its first stage); dr keeps
   // the full transform for the j-symmetric table positions; rev_r = position
   // -> frequency (natural-order gathers)
-  int r1;
+  int r1, ilv;
   FftDesc dsub;
   const cplx<T>* tw_sub;
   const int* rev_r;
@@ -151,6 +152,23 @@ void launch_convert(long n, const double* in, T* out, cudaStream_t s);
 template <typename T>
 void launch_ground_metrics(const T* v, int batch, int nr, int nt, int row, int k0, int n,
                            const double* x, double* out, cudaStream_t s);
+
+// splitting.cu (splitting baseline, float64; -fmad=false)
+void launch_split_prep(const double* v, int n, int nt, int ldn, double* vT, double* sT,
+                       cudaStream_t s);
+void launch_split_diffraction(const double* vT, const double* sT, int n, int nt, int ldn,
+                              double gamma, const double* w, const double* up, const double* dg,
+                              double* out, double* gline, cudaStream_t s);
+bool split_line_in_smem(int n);
+void launch_split_burgers(const double* v, int n, int nt, double B, double ratio, double* out,
+                          cudaStream_t s);
+void launch_godunov_flux(long n, const double* ul, const double* ur, double B, double* out,
+                         cudaStream_t s);
+void launch_split_axial(double2* spec, int n, int kk, int ld, const double* upar, double ds,
+                        double A, double theta_span, cudaStream_t s);
+void launch_split_transverse(const double* v, int n, int nt, const double* up, const double* dus,
+                             const double* dur, double ds, double dr, double* out,
+                             unsigned long long* vmax, cudaStream_t s);
 
 // tables.cu (compiled with -fmad=false so the z / exp / phi arithmetic
 // rounds like numpy's)

@@ -185,7 +185,10 @@ __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R, SP
   for (int idx = threadIdx.x; idx < kk * R && !(a.debug & 4); idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r * jstep;
     V* slot = &z[r * rs + pidx(a.dh, k)];
-    if (j < nr) cp_async_c(slot, &src[(size_t)k * ld + j]);
+    // SPLIT: sub-column position r msub + i is stored interleaved at i r1 + r
+    // (the R values of one k are adjacent: whole 32-byte sectors)
+    if (SPLIT) cp_async_c(slot, &src[(size_t)k * ld + (a.ilv ? j0 * R + r : j)]);
+    else if (j < nr) cp_async_c(slot, &src[(size_t)k * ld + j]);
     else *slot = mk<V>(0, 0);
   }
   cp_async_wait_all();
@@ -246,8 +249,10 @@ template <typename T, int R>
 __device__ __forceinline__ void r2c_post_split(const cplx<T>* z, const ThetaArgs<T>& a, int rs,
                                                int mem, int i) {
   using V = cplx<T>;
-  const int m = a.g.m, ld = a.g.ld, ms = a.msub;
-  V* dst = a.spec_out + (size_t)mem * a.g.kk * ld + i;
+  const int m = a.g.m, ld = a.g.ld;
+  // position q msub + i stored at i R + q (interleaved, ThetaArgs::ilv) or at q msub + i
+  V* dst = a.spec_out + (size_t)mem * a.g.kk * ld + (a.ilv ? (size_t)i * R : (size_t)i);
+  const int qs = a.ilv ? 1 : a.msub;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
   V w[R];
@@ -272,13 +277,13 @@ __device__ __forceinline__ void r2c_post_split(const cplx<T>* z, const ThetaArgs
 #pragma unroll
     for (int q = 1; q < R; ++q) xk[q] = cmul(xk[q], w[q]);
 #pragma unroll
-    for (int q = 0; q < R; ++q) dst[(size_t)k * ld + q * ms] = xk[q];
+    for (int q = 0; q < R; ++q) dst[(size_t)k * ld + q * qs] = xk[q];
     if (2 * k != m) {
       bfly<R, false>(xm);
 #pragma unroll
       for (int q = 1; q < R; ++q) xm[q] = cmul(xm[q], w[q]);
 #pragma unroll
-      for (int q = 0; q < R; ++q) dst[(size_t)(m - k) * ld + q * ms] = xm[q];
+      for (int q = 0; q < R; ++q) dst[(size_t)(m - k) * ld + q * qs] = xm[q];
     }
   }
 }
@@ -606,14 +611,17 @@ __global__ void __launch_bounds__(256, rho_sub_min_blocks<T>()) k_rho_sub(const 
       if (a.vh) a.vh[sub + p] = val;
     }
   } else {
-    const V* src = a.in + sub;
-    for (int j = threadIdx.x; j < ms; j += blockDim.x) cp_async_c(&x[pidx(d, j)], &src[j]);
+    // transit arrays (theta passes <-> rho pass) hold position q1 msub + j at
+    // j r1 + q1: the r1 sub-columns of a column interleave
+    const int js = a.ilv ? r1 : 1;
+    const V* src = a.in + (a.ilv ? row + q1 : sub);
+    for (int j = threadIdx.x; j < ms; j += blockDim.x) cp_async_c(&x[pidx(d, j)], &src[(size_t)j * js]);
     cp_async_wait_all();
   }
   if (a.zero_bits && blockIdx.y == 0 && threadIdx.x == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
   __syncthreads();
   if (MODE != RHO_INV_NAT) fft_forward(x, d, 1, 0, a.tw_sub);
-  if (MODE == RHO_FWD_DR) {
+  if (MODE == RHO_FWD_DR) {  // plain position order (RHO_REV2NAT permutes next)
     V* dst = a.out + sub;
     for (int p = threadIdx.x; p < ms; p += blockDim.x) dst[p] = x[pidx(d, p)];
     return;
@@ -624,8 +632,9 @@ __global__ void __launch_bounds__(256, rho_sub_min_blocks<T>()) k_rho_sub(const 
                          q1 * ms);
   __syncthreads();
   fft_inverse(x, d, 1, 0, a.tw_sub);
-  V* dst = a.out + sub;
-  for (int j = threadIdx.x; j < ms; j += blockDim.x) dst[j] = x[pidx(d, j)];
+  const int js = a.ilv ? r1 : 1;
+  V* dst = a.out + (a.ilv ? row + q1 : sub);
+  for (int j = threadIdx.x; j < ms; j += blockDim.x) dst[(size_t)j * js] = x[pidx(d, j)];
   if (a.step_ctr && mem == 0 && blockIdx.y == 0 && threadIdx.x == 0) *a.step_ctr += 1;
 }
 

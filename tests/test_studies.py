@@ -42,9 +42,16 @@ def oracle_solver(monkeypatch, oracle):
 
     def run(solver, config, fields, threads=1, guard=10.0, snapshot_sigmas=None, **kw):
         _, rho, theta = nw.build_axes(config)
-        v0 = nw.initial_nwave(rho, theta, config.A, config.B).values
-        r = oracle.march(config, v0, fields, scheme=solver, guard=guard,
-                         snapshot_sigmas=snapshot_sigmas)
+        if solver == "splitting":
+            from oracle import splitting_oracle
+
+            v0 = nw.initial_nwave(nw.rho_nodes_closed(config), theta, config.A, config.B).values
+            r = splitting_oracle.march(config, v0, fields, snapshot_sigmas=snapshot_sigmas,
+                                       guard=guard)
+        else:
+            v0 = nw.initial_nwave(rho, theta, config.A, config.B).values
+            r = oracle.march(config, v0, fields, scheme=solver, guard=guard,
+                             snapshot_sigmas=snapshot_sigmas)
         if r.failed_sigma is not None:
             raise nw.InstabilityError(r.failed_sigma, r.max_abs_v)
         return SimpleNamespace(final=nw.Field2D(r.final),
@@ -78,7 +85,8 @@ def test_convergence_study_logic_vs_reference(gs, oracle_solver, solver, roi):
 
 def test_compare_solvers_logic_vs_reference(gs, oracle_solver):
     cfg, _, fields = study_setup(gs)
-    rep = studies.compare_solvers(cfg, fields, [0.6, 1.2, 2.4], trace_sigma=2.4, trace_rho=144.0)
+    rep = studies.compare_solvers(cfg, fields, [0.6, 1.2, 2.4], trace_sigma=2.4, trace_rho=144.0,
+                                  solver_pair=("expeuler", "exprk22"))
     ref = gs["compare"]
     for c, (s, rel, amp) in zip(rep.checkpoints, ref["checkpoints"]):
         assert c.sigma == s
@@ -106,10 +114,10 @@ def test_convergence_rate_and_errors(gs):
         studies.convergence_study(cfg, [4], gs["n_ref"])
     with pytest.raises(ValueError, match="sigma rows"):
         studies.convergence_study(cfg, [4], 16, fields_master=master)
-    with pytest.raises(ValueError, match="splitting"):
-        studies.convergence_study(cfg, [4], gs["n_ref"], solver="splitting", fields_master=master)
-    with pytest.raises(ValueError, match="splitting"):
-        studies.compare_solvers(cfg, fields, [1.2], solver_pair=("splitting", "exprk22"))
+    with pytest.raises(ValueError, match="unknown solver"):
+        studies.convergence_study(cfg, [4], gs["n_ref"], solver="godunov", fields_master=master)
+    with pytest.raises(ValueError, match="unknown solver"):
+        studies.compare_solvers(cfg, fields, [1.2], solver_pair=("rk4", "exprk22"))
 
 
 def test_unstable_run_breaks_rate_chain(gs, monkeypatch):
@@ -175,3 +183,24 @@ def test_snapshot_writer_names(tmp_path):
                      "V_sigma0001p000.bin", "V_sigma0001p000.csv"]
     vals, _, _, s = fieldio.read_grid_binary(paths[0])
     assert s == 0.5 and np.array_equal(vals, np.ones((4, 6)))
+
+
+def test_compare_solvers_default_pair_splitting_vs_reference(oracle_solver):
+    """The reference's default pair (splitting, exprk22) on the oracle marches
+    equals the reference's own report (tests/golden/golden_splitting.json)."""
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "golden_splitting.json")) as fh:
+        ref = json.load(fh)["compare"]
+    cfg = nw.DomainConfig(N_rho=250, N_theta=112, N_sigma=40, Sigma=16.0)
+    sig, _, _ = nw.build_axes(cfg)
+    spec = nw.sample_modes(nw.TurbulenceParams(seed=5))
+    fl = nw.evaluate_fields(spec, spec.lam, sig, nw.rho_nodes_closed(cfg))
+    rep = studies.compare_solvers(cfg, fl, [8.0, 16.0], trace_sigma=16.0, trace_rho=144.0)
+    for c, (s, rel, amp) in zip(rep.checkpoints, ref["checkpoints"]):
+        assert c.sigma == s
+        assert c.rel_l2_roi == pytest.approx(rel, rel=1e-9)
+        assert c.amplitude_ratio == pytest.approx(amp, rel=1e-12)
+    assert rep.overshoot_splitting == pytest.approx(ref["overshoot_splitting"], rel=1e-9)
+    assert rep.overshoot_exprk22 == pytest.approx(ref["overshoot_exprk22"], rel=1e-9)
