@@ -575,6 +575,17 @@ def main():
     res32 = None
     if not args.no_fp32:
         res32 = time_precision(cfg, args.config, "single", args.steps, warmup, world, rank, local)
+    slab = None
+    if world > 1 and args.config != "c4":
+        # the single large grid (BASELINE C5) over all ranks: rho slabs with
+        # NCCL all-to-all transposes, MAX all-reduce and the halo ring (slab.py)
+        c5, c5_desc = workload("c5")
+        ks = min(args.steps, 20)
+        rs = time_slab(c5, ks, warmup, world, rank, local)
+        slab = {"workload": c5_desc, "value": rs["value"], "unit": UNIT,
+                "ms_per_step": rs["ms_per_step"], "steps": ks, "n_ranks": world,
+                "scaling": "strong", "dtype": "f64", "clocks": rs["clocks"],
+                "parallelism": f"rho-slab x{world} (NCCL all-to-all + MAX all-reduce + halo ring)"}
     e2e = e2e32 = None
     if not args.no_e2e:
         e2e = e2e_precision(cfg, args.config, "double", args.steps, world, rank, local)
@@ -600,6 +611,8 @@ def main():
                   "e2e": e2e32} if res32 else None),
         "impl": "b200",
     }
+    if slab is not None:
+        line["slab_c5"] = slab
     print(json.dumps(line), flush=True)
 
 

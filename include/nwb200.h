@@ -98,11 +98,15 @@ int nwb_plan_store_physical(nwb_plan* plan, void* v_dev, double* max_abs_host);
  *     device buffers (batch, n_rho, n_theta).
  *   max_abs_host: [batch * n_steps] max|V_n| per member and step (or NULL).
  *   step_ms_host: [n_steps * 3] = (step, nonlinear, linear) device ms from
- *     CUDA events, or NULL (then steps are replayed from a CUDA graph).
+ *     CUDA events recorded by the replayed step graph, or NULL (graph replay
+ *     without events).
  *   guard: stop with NWB_EINSTABILITY at the first step whose max|V_n| is
- *     non-finite or > guard; *fail_step, *fail_member, *fail_value say where.
- *   max_seconds > 0: stop with NWB_EBUDGET once the host wall clock exceeds it
- *     (checked at synchronisation points); *fail_step = steps completed. */
+ *     non-finite or > guard; *fail_step, *fail_member, *fail_value say where
+ *     (the message carries "step=<n> member=<i> max_abs=<v>").
+ *   max_seconds >= 0: stop with NWB_EBUDGET once the host wall clock exceeds
+ *     it (checked after step 1 and then every 8 steps, so a zero budget stops
+ *     after step 1 like exprk.py:303-306); < 0: no budget.
+ *     *fail_step = absolute steps completed. */
 int nwb_march(nwb_plan* plan, int scheme, int n0, int n_steps, double guard,
               double max_seconds, const int* snap_steps, int n_snap,
               void* const* snap_bufs_dev, double* max_abs_host, float* step_ms_host,
@@ -151,6 +155,10 @@ int nwb_slab_create(nwb_slab** slab, int n_rho, int n_theta, int j0, int rows, i
 int nwb_slab_destroy(nwb_slab* slab);
 int nwb_slab_set_stream(nwb_slab* slab, void* stream);
 int nwb_slab_layout(const nwb_slab* slab, int* ld_rows, int* ld_rho);
+/* rho-side transit layout of nwb_slab_rho's bt / out: with n_blocks > 0 the
+ * rank-b block (modes x rows_b, rows [row_starts[b], row_starts[b+1])) is
+ * stored contiguously at modes * row_starts[b] -- the all-to-all segments. */
+int nwb_slab_set_blocks(nwb_slab* slab, int n_blocks, const int* row_starts);
 int nwb_slab_set_coeffs(nwb_slab* slab, const double* u_par, const double* u_perp,
                         const double* du_drho, int n_rows, int ld, int on_device);
 /* red == NULL: plain inverse transform (no reductions). */

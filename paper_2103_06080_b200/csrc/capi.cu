@@ -1109,6 +1109,7 @@ struct nwb_slab {
   int nr = 0, nt = 0, m = 0, kk = 0;  // global grid
   int j0 = 0, rows = 0, ld_rows = 0;  // owned rho rows (theta side)
   int k0 = 0, modes = 0, ld_rho = 0;  // owned theta modes (rho side)
+  int blk_n = 0, blk_start[17] = {};   // rho-side transit blocks (nwb_slab_set_blocks)
   double d_sigma = 0, rho_span = 0, theta_span = 0, A = 0, B = 0, eps = 0;
   FftDesc dr{}, dh{};
   FftPlanHost plan_r, plan_h;
@@ -1291,6 +1292,8 @@ template <typename T> int slab_rho_impl(nwb_slab* s, int mode, const void* bt, v
   q.P2 = (const cplx<T>*)s->P2;
   q.ds = (T)s->d_sigma;
   q.prefetch = 100;
+  q.blk_n = s->blk_n;
+  for (int b = 0; b <= s->blk_n && b < 17; ++b) q.blk_start[b] = s->blk_start[b];
   launch_rho<T>(q, mode, s->rho_threads, s->stream);
   CHECK_LAUNCH("slab rho");
   return NWB_OK;
@@ -1504,7 +1507,9 @@ int nwb_slab_create(nwb_slab** out, int n_rho, int n_theta, int j0, int rows, in
   nwb_slab* s = new nwb_slab();
   s->device = device; s->prec = precision;
   s->nr = n_rho; s->nt = n_theta; s->m = n_theta / 2; s->kk = kk;
-  s->j0 = j0; s->rows = rows; s->ld_rows = (rows + 7) / 8 * 8;
+  // theta-side spectra (kk, rows) are unpadded: the block a rank receives
+  // from (or sends to) rank r is then one contiguous segment
+  s->j0 = j0; s->rows = rows; s->ld_rows = rows;
   s->k0 = k0; s->modes = modes; s->ld_rho = (n_rho + 7) / 8 * 8;
   s->d_sigma = d_sigma; s->rho_span = rho_span; s->theta_span = theta_span;
   s->A = A; s->B = B; s->eps = eps;
@@ -1546,6 +1551,20 @@ int nwb_slab_destroy(nwb_slab* s) {
 int nwb_slab_set_stream(nwb_slab* s, void* stream) {
   if (!s) return fail(NWB_EINVAL, "null slab");
   s->stream = stream ? (cudaStream_t)stream : s->own_stream;
+  return NWB_OK;
+}
+
+int nwb_slab_set_blocks(nwb_slab* s, int n_blocks, const int* row_starts) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (n_blocks < 0 || n_blocks > 16) return fail(NWB_EINVAL, "slab blocks: 0 .. 16 ranks");
+  if (n_blocks > 0) {
+    if (row_starts[0] != 0 || row_starts[n_blocks] != s->nr)
+      return fail(NWB_EINVAL, "slab blocks must partition the rho rows");
+    for (int b = 0; b < n_blocks; ++b)
+      if (row_starts[b + 1] < row_starts[b]) return fail(NWB_EINVAL, "slab blocks out of order");
+    for (int b = 0; b <= n_blocks; ++b) s->blk_start[b] = row_starts[b];
+  }
+  s->blk_n = n_blocks;
   return NWB_OK;
 }
 

@@ -102,6 +102,12 @@ template <typename T> struct RhoArgs {
   // the msub-point transform (the full plan without its first stage); dr keeps
   // the full transform for the j-symmetric table positions; rev_r = position
   // -> frequency (natural-order gathers)
+  // slab transit layout (multi-GPU, slab.py): in / out hold, per destination
+  // or source rank b with rho rows [blk_start[b], blk_start[b+1]), the block
+  // (local modes x rows_b) contiguously at kk * blk_start[b] -- the
+  // all-to-all's segments, so it moves them without packing copies
+  int blk_n;
+  int blk_start[17];
   int r1, ilv;
   FftDesc dsub;
   const cplx<T>* tw_sub;

@@ -48,6 +48,14 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 #ifndef NWB_THETA_MINB64
 #define NWB_THETA_MINB64 2
 #endif
+// unroll of the theta pre / post loops (independent iterations: several
+// table loads and shared-memory gathers in flight per thread)
+#ifndef NWB_POST_UNROLL
+#define NWB_POST_UNROLL 1
+#endif
+#define NWB_PRAGMA_(x) _Pragma(#x)
+#define NWB_PRAGMA(x) NWB_PRAGMA_(x)
+#define NWB_UNROLL(n) NWB_PRAGMA(unroll n)
 #ifndef NWB_RHO_THREADS_LB
 #define NWB_RHO_THREADS_LB 512
 #endif
@@ -96,6 +104,7 @@ __device__ __forceinline__ void c2r_pre(cplx<T>* z, const ThetaArgs<T>& a, int r
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     V* zr = z + r * rs;
+    NWB_UNROLL(NWB_POST_UNROLL)
     for (int k = threadIdx.x; k < npairs; k += blockDim.x) {
       const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
       V xk = zr[sk];
@@ -127,6 +136,7 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
     V* drow = reinterpret_cast<V*>(dst + (size_t)j * a.g.nt);
     T hi = -INFINITY, lo = INFINITY;
     bool nan = false;
+    NWB_UNROLL(NWB_POST_UNROLL)
     for (int n = threadIdx.x; n < m; n += blockDim.x) {
       const V zz = zr[pidx(a.dh, __ldg(&a.pos_h[n]))];
       const T v0 = zz.x * scale, v1 = zz.y * scale;
@@ -225,6 +235,7 @@ __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
+  NWB_UNROLL(NWB_POST_UNROLL)
   for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
     if (j >= jend) continue;
@@ -508,6 +519,16 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
   }
 }
 
+// element j of column k of the in / out arrays (RhoArgs::blk_n: slab blocks)
+template <typename T>
+__device__ __forceinline__ size_t rho_io(const RhoArgs<T>& a, size_t row, int k, int j) {
+  if (!a.blk_n) return row + j;
+  int b = 0;
+  while (b + 1 < a.blk_n && j >= a.blk_start[b + 1]) ++b;
+  const int st = a.blk_start[b], len = a.blk_start[b + 1] - st;
+  return (size_t)a.g.kk * st + (size_t)k * len + (j - st);
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho(const RhoArgs<T> a) {
   using V = cplx<T>;
@@ -549,6 +570,9 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
       x[pidx(a.dr, p)] = val;
       if (a.vh) a.vh[row + p] = val;
     }
+  } else if (a.blk_n) {
+    for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &a.in[rho_io(a, row, k, j)]);
+    cp_async_wait_all();
   } else if (!(a.debug & 4)) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &src[j]);
     cp_async_wait_all();
@@ -571,7 +595,9 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   __syncthreads();
   if (!(a.debug & 1)) fft_inverse(x, a.dr, 1, 0, a.tw_r);
   V* dst = a.out + row;
-  if (!(a.debug & 4))
+  if (a.blk_n)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) a.out[rho_io(a, row, k, j)] = x[pidx(a.dr, j)];
+  else if (!(a.debug & 4))
     for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
 }

@@ -21,7 +21,7 @@ import numpy as np
 
 STAGE_BYTES = 32 << 20
 
-_staging: dict = {}
+_free_pairs: dict = {}  # device index -> list of idle staging pairs
 _staging_lock = threading.Lock()
 
 
@@ -31,46 +31,55 @@ def _torch():
     return torch
 
 
-def _staging_pair(key):
-    """Two page-locked STAGE_BYTES chunks per (device, user) key, allocated once."""
+def _acquire_pair(dev: int):
+    """An idle pair of page-locked STAGE_BYTES chunks for device ``dev``
+    (allocated on first need; as many exist as copies ever ran at once)."""
     torch = _torch()
     with _staging_lock:
-        bufs = _staging.get(key)
-        if bufs is None:
-            bufs = [torch.empty(STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
-            _staging[key] = bufs
-        return bufs
+        idle = _free_pairs.setdefault(dev, [])
+        if idle:
+            return idle.pop()
+    return [torch.empty(STAGE_BYTES, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
 
 
-def copy_to_host(src, out: np.ndarray, stream=None, key="main") -> np.ndarray:
+def _release_pair(dev: int, pair):
+    with _staging_lock:
+        _free_pairs.setdefault(dev, []).append(pair)
+
+
+def copy_to_host(src, out: np.ndarray, stream=None) -> np.ndarray:
     """Copy device tensor ``src`` into numpy ``out`` (same element count; dtype
-    widened on the host) through the staging pair, on ``stream`` (default:
-    the current stream), after the work already queued there."""
+    widened on the host) through a staging pair, on ``stream`` (default: the
+    current stream), after the work already queued there.  Each copy holds
+    its own pair for its duration, so concurrent copies (studies run several
+    marches at once; snapshot drains run beside the march) never share one."""
     torch = _torch()
     flat = src.reshape(-1)
     dst = out.reshape(-1)
     if flat.numel() != dst.size:
         raise ValueError("copy_to_host: element counts differ")
     stream = stream or torch.cuda.current_stream(src.device)
-    es = flat.element_size()
-    per = STAGE_BYTES // es
-    bufs = _staging_pair((src.device.index, key))
-    views = [b.view(flat.dtype) for b in bufs]
-    pending = []  # (event, k, start, end)
-    with torch.cuda.stream(stream):
-        for i, s in enumerate(range(0, flat.numel(), per)):
-            e, k = min(flat.numel(), s + per), i & 1
-            if len(pending) == 2:  # buffer k is still held by chunk i-2: drain it
-                ev, kk, s0, e0 = pending.pop(0)
+    per = STAGE_BYTES // flat.element_size()
+    bufs = _acquire_pair(src.device.index)
+    try:
+        views = [b.view(flat.dtype) for b in bufs]
+        pending = []  # (event, k, start, end)
+        with torch.cuda.stream(stream):
+            for i, s in enumerate(range(0, flat.numel(), per)):
+                e, k = min(flat.numel(), s + per), i & 1
+                if len(pending) == 2:  # buffer k is still held by chunk i-2: drain it
+                    ev, kk, s0, e0 = pending.pop(0)
+                    ev.synchronize()
+                    np.copyto(dst[s0:e0], views[kk][: e0 - s0].numpy(), casting="unsafe")
+                views[k][: e - s].copy_(flat[s:e], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                pending.append((ev, k, s, e))
+            for ev, kk, s0, e0 in pending:
                 ev.synchronize()
                 np.copyto(dst[s0:e0], views[kk][: e0 - s0].numpy(), casting="unsafe")
-            views[k][: e - s].copy_(flat[s:e], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-            pending.append((ev, k, s, e))
-        for ev, kk, s0, e0 in pending:
-            ev.synchronize()
-            np.copyto(dst[s0:e0], views[kk][: e0 - s0].numpy(), casting="unsafe")
+    finally:
+        _release_pair(src.device.index, bufs)
     return out
 
 
@@ -121,7 +130,7 @@ class SnapshotStreamer:
             with torch.cuda.device(self.plan.device):
                 self.copy_stream.wait_event(ready)
                 out = np.empty(tuple(slot.shape), dtype=np.float64)
-                copy_to_host(slot, out, self.copy_stream, key=("snap", k))
+                copy_to_host(slot, out, self.copy_stream)
                 self.results[key] = out
         except BaseException as exc:  # surfaced by capture() / finish()
             self.errors.append(exc)

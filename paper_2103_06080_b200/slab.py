@@ -19,6 +19,16 @@ tests plug in a numpy implementation to check the decomposition logic.
 The reduction values are IEEE bit patterns of non-negative doubles held in an
 int64 tensor, so the MAX all-reduce is exact and order-independent (the
 march stays bitwise reproducible for any G).
+
+Transit layouts are chosen so the all-to-alls move the arrays in place:
+the theta-side spectrum ``spec_rows`` is (kk, rows) unpadded, so the block
+exchanged with rank r (its modes x my rows) is one contiguous segment; the
+rho-side ``bt_rho`` / ``t_rho`` are block-major -- the block of rank b's rows
+(my modes x rows_b) is contiguous at modes * row_start_b (``nwb_slab_set_blocks``;
+the rho kernels read and write that layout).  Both sides are then exactly
+``all_to_all_single``'s rank-ordered segments: no packing or unpacking
+copies.  The divergence guard is kept on the device (a per-step history of
+the all-reduced max|V|) and checked on the host every ``GUARD_EVERY`` steps.
 """
 
 from __future__ import annotations
@@ -59,6 +69,28 @@ def _dist():
     return dist
 
 
+def rank_row_starts(n_rho: int, world: int) -> list[int]:
+    """Row partition of the rho axis over ``world`` ranks (shard_members)."""
+    return [shard_members(n_rho, world, r).start for r in range(world)] + [n_rho]
+
+
+def blocks_to_natural(flat, modes: int, starts):
+    """Block-major rho-side layout -> (modes, n_rho) natural layout."""
+    nat = flat.new_empty((modes, starts[-1]))
+    for b in range(len(starts) - 1):
+        a, e = starts[b], starts[b + 1]
+        nat[:, a:e] = flat[modes * a:modes * e].reshape(modes, e - a)
+    return nat
+
+
+def natural_to_blocks(nat, flat, starts):
+    """(modes, n_rho) natural layout -> block-major rho-side layout (in place)."""
+    modes = nat.shape[0]
+    for b in range(len(starts) - 1):
+        a, e = starts[b], starts[b + 1]
+        flat[modes * a:modes * e] = nat[:, a:e].reshape(-1)
+
+
 class _Comm:
     """Collectives of the slab march (or local copies for a single rank)."""
 
@@ -66,27 +98,20 @@ class _Comm:
         self.group = group
         self.geo = geo
 
-    def all_to_all(self, sends, recv_shapes, like):
-        """sends[s]: tensor for rank s; returns list of tensors received from each rank."""
+    def exchange(self, out_flat, in_flat, out_splits, in_splits):
+        """all_to_all_single on flat complex buffers whose rank-ordered
+        segments are the blocks (in place, no packing)."""
         import torch
 
-        G = self.geo.world
-        if G == 1:
-            return [sends[0].clone()]
-        real = torch.is_complex(like)
-        flat_in = torch.cat([(torch.view_as_real(t) if real else t).reshape(-1) for t in sends])
-        in_splits = [t.numel() * (2 if real else 1) for t in sends]
-        out_splits = [int(np.prod(sh)) * (2 if real else 1) for sh in recv_shapes]
-        flat_out = torch.empty(sum(out_splits), dtype=flat_in.dtype, device=flat_in.device)
-        _dist().all_to_all_single(flat_out, flat_in, out_splits, in_splits, group=self.group)
-        outs, o = [], 0
-        for sh, n in zip(recv_shapes, out_splits):
-            chunk = flat_out[o:o + n]
-            o += n
-            if real:
-                chunk = torch.view_as_complex(chunk.reshape(*sh, 2))
-            outs.append(chunk.reshape(sh))
-        return outs
+        if self.geo.world == 1:
+            out_flat.copy_(in_flat)
+            return
+        real = torch.is_complex(in_flat)
+        o = torch.view_as_real(out_flat).reshape(-1) if real else out_flat
+        i = torch.view_as_real(in_flat).reshape(-1) if real else in_flat
+        f = 2 if real else 1
+        _dist().all_to_all_single(o, i, [f * n for n in out_splits], [f * n for n in in_splits],
+                                  group=self.group)
 
     def max_(self, t):
         if self.geo.world > 1:
@@ -152,11 +177,15 @@ class GpuSlabOps:
             ldr, ldp = ctypes.c_int(), ctypes.c_int()
             check(self.lib.nwb_slab_layout(self._h, ctypes.byref(ldr), ctypes.byref(ldp)), "layout")
             z = lambda *shape, dt: torch.zeros(shape, dtype=dt, device=self.dev)
-            self.spec_rows = z(geo.kk, ldr.value, dt=self.cdt)
+            assert ldr.value == len(rows)  # unpadded theta-side spectrum
+            starts = rank_row_starts(geo.n_rho, geo.world)
+            sarr = (ctypes.c_int * len(starts))(*starts)
+            check(self.lib.nwb_slab_set_blocks(self._h, geo.world, sarr), "slab blocks")
+            self.spec_rows = z(geo.kk, len(rows), dt=self.cdt)
             self.v_ext = z(len(rows) + 6, geo.n_theta, dt=self.rdt)
             self.b = z(len(rows), geo.n_theta, dt=self.rdt)
-            self.bt_rho = z(len(modes), ldp.value, dt=self.cdt)
-            self.t_rho = z(len(modes), ldp.value, dt=self.cdt)
+            self.bt_rho = z(len(modes) * geo.n_rho, dt=self.cdt)  # block-major transit
+            self.t_rho = z(len(modes) * geo.n_rho, dt=self.cdt)
             self.vh = z(len(modes), ldp.value, dt=self.cdt)
             self.u = z(len(modes), ldp.value, dt=self.cdt)
             self.red = z(2, dt=torch.int64)
@@ -214,8 +243,12 @@ class GpuSlabOps:
 class SlabMarch:
     """Drives the per-slab kernels and the collectives (see module docstring)."""
 
+    GUARD_EVERY = 16
+
     def __init__(self, config: DomainConfig, fields, precision: str = "double", group=None,
                  ops=None, device=None, max_steps: int | None = None):
+        import torch
+
         self.cfg = config
         if group is not None or _dist().is_available() and _dist().is_initialized():
             world, rank = _dist().get_world_size(group), _dist().get_rank(group)
@@ -227,28 +260,25 @@ class SlabMarch:
         self.n_steps = config.N_sigma if max_steps is None else min(config.N_sigma, max_steps)
         self.ops.set_coeffs(fields, self.n_steps + 1)
         self.max_abs = []
+        # per-step all-reduced max|V| (IEEE bits), on the ops' device
+        self.hist = torch.zeros(max(self.n_steps, 1), dtype=torch.int64, device=self.ops.red.device)
+        self._checked = 0
+        g = self.geo
+        rows_me, modes_me = len(g.rows()), len(g.modes())
+        # all-to-all segment sizes (complex elements), rank order
+        self._r2t_in = [modes_me * len(g.rows(s)) for s in range(g.world)]
+        self._r2t_out = [len(g.modes(r)) * rows_me for r in range(g.world)]
+        self._t2r_in = [len(g.modes(s)) * rows_me for s in range(g.world)]
+        self._t2r_out = [modes_me * len(g.rows(r)) for r in range(g.world)]
 
-    # -- layout changes ----------------------------------------------------
+    # -- layout changes (in place: see the module docstring) ----------------
     def _rho_to_theta(self):
-        g, o = self.geo, self.ops
-        me_rows = g.rows()
-        sends = [o.t_rho[:, g.rows(s).start:g.rows(s).stop].contiguous() for s in range(g.world)]
-        shapes = [(len(g.modes(r)), len(me_rows)) for r in range(g.world)]
-        recv = self.comm.all_to_all(sends, shapes, o.t_rho)
-        for r, blk in enumerate(recv):
-            m = g.modes(r)
-            o.spec_rows[m.start:m.stop, :len(me_rows)] = blk
+        o = self.ops
+        self.comm.exchange(o.spec_rows.reshape(-1), o.t_rho.reshape(-1), self._r2t_out, self._r2t_in)
 
     def _theta_to_rho(self):
-        g, o = self.geo, self.ops
-        n_me = len(g.rows())
-        sends = [o.spec_rows[g.modes(s).start:g.modes(s).stop, :n_me].contiguous()
-                 for s in range(g.world)]
-        shapes = [(len(g.modes()), len(g.rows(r))) for r in range(g.world)]
-        recv = self.comm.all_to_all(sends, shapes, o.spec_rows)
-        for r, blk in enumerate(recv):
-            rr = g.rows(r)
-            o.bt_rho[:, rr.start:rr.stop] = blk
+        o = self.ops
+        self.comm.exchange(o.bt_rho.reshape(-1), o.spec_rows.reshape(-1), self._t2r_out, self._t2r_in)
 
     # -- march -------------------------------------------------------------
     def load(self, v0_rows):
@@ -262,33 +292,47 @@ class SlabMarch:
         self._theta_to_rho()
         o.rho(RHO_INIT)
 
-    def _stage(self, row: int, mode: int, guard_slot: bool):
+    def _stage(self, row: int, mode: int, guard_step: int | None):
         o = self.ops
         self._rho_to_theta()
         o.red.zero_()
         o.c2r(row, reduce=True)
         self.comm.max_(o.red)
-        if guard_slot:
-            self.max_abs.append(float(o.red_values()[1]))
+        if guard_step is not None:
+            self.hist[guard_step] = o.red[1]  # device copy: no host sync per step
         self.comm.halo(o.v_ext, len(self.geo.rows()))
         o.weno(row)
         o.r2c()
         self._theta_to_rho()
         o.rho(mode)
 
+    def _check_guard(self, upto: int, guard: float):
+        """Host check of the guard history for steps [checked, upto)."""
+        if upto <= self._checked:
+            return
+        vals = self.hist[self._checked:upto].cpu().numpy().view(np.float64)
+        for i, m in enumerate(vals):
+            m = float(m)
+            self.max_abs.append(m)
+            if not np.isfinite(m) or m > guard:
+                raise InstabilityError((self._checked + i) * self.cfg.d_sigma, m)
+        self._checked = upto
+
     def march(self, scheme: str = "exprk22", guard: float = 10.0, n0: int = 0,
               steps: int | None = None):
         """March ``steps`` steps from absolute step ``n0`` (default: the whole run)."""
         stop = self.n_steps if steps is None else min(self.n_steps, n0 + steps)
+        if n0 != self._checked:
+            self._checked = n0
         for n in range(n0, stop):
             if scheme == "exprk22":
-                self._stage(n, RHO_STAGE1, True)
-                self._stage(n + 1, RHO_STAGE2, False)
+                self._stage(n, RHO_STAGE1, n)
+                self._stage(n + 1, RHO_STAGE2, None)
             else:
-                self._stage(n, RHO_EULER, True)
-            m = self.max_abs[-1]
-            if not np.isfinite(m) or m > guard:
-                raise InstabilityError(n * self.cfg.d_sigma, m)
+                self._stage(n, RHO_EULER, n)
+            if (n + 1 - n0) % self.GUARD_EVERY == 0:
+                self._check_guard(n + 1, guard)
+        self._check_guard(stop, guard)
         return self
 
     def final_rows(self):

@@ -1,13 +1,16 @@
 """TEST INFRASTRUCTURE: numpy per-slab ops with the GpuSlabOps interface, so the
 rho-slab decomposition (paper_2103_06080_b200/slab.py) can be checked on CPU
-ranks over gloo.  Conventions: spec_rows = rfft_theta of the owned rows
-(transposed, (kk, rows)), t_rho = ifft_rho of the state spectrum (own modes,
-natural rho order); the arithmetic restates exprk.py:151-178 and weno.py."""
+ranks over gloo.  Conventions (those of the GPU slab): spec_rows = rfft_theta
+of the owned rows (transposed, (kk, rows)); bt_rho / t_rho in the block-major
+transit layout of slab.py (block of rank b's rows contiguous at modes *
+row_start_b), holding rfft_theta of b / ifft_rho of the state spectrum; the
+arithmetic restates exprk.py:151-178 and weno.py."""
 
 import numpy as np
 import torch
 
 from oracle import nwave_oracle as O
+from paper_2103_06080_b200.slab import blocks_to_natural, natural_to_blocks, rank_row_starts
 
 TWO_PI = 2.0 * np.pi
 
@@ -26,8 +29,9 @@ class NumpySlabOps:
         self.spec_rows = z(geo.kk, len(rows), dt=c)
         self.v_ext = z(len(rows) + 6, config.N_theta, dt=r)
         self.b = z(len(rows), config.N_theta, dt=r)
-        self.bt_rho = z(len(modes), config.N_rho, dt=c)
-        self.t_rho = z(len(modes), config.N_rho, dt=c)
+        self.bt_rho = z(len(modes) * config.N_rho, dt=c)
+        self.t_rho = z(len(modes) * config.N_rho, dt=c)
+        self.starts = rank_row_starts(config.N_rho, geo.world)
         self.vh = z(len(modes), config.N_rho, dt=c)
         self.u = z(len(modes), config.N_rho, dt=c)
         self.red = z(2, dt=torch.int64)
@@ -68,8 +72,13 @@ class NumpySlabOps:
         x = (self.b if src is None else src).numpy()
         self.spec_rows.copy_(torch.from_numpy(np.fft.rfft(x, axis=1).T.copy()))
 
+    def _put_t(self, nat):
+        natural_to_blocks(torch.from_numpy(np.ascontiguousarray(nat)), self.t_rho, self.starts)
+
     def rho(self, mode):
-        bh = np.fft.fft(self.bt_rho.numpy(), axis=1)
+        nmodes = len(self.geo.modes())
+        bt = blocks_to_natural(self.bt_rho, nmodes, self.starts).numpy()
+        bh = np.fft.fft(bt, axis=1)
         ds = self.cfg.d_sigma
         vh, u = self.vh.numpy(), self.u.numpy()
         if mode == 3:
@@ -77,14 +86,14 @@ class NumpySlabOps:
         elif mode == 0:
             ev = self.E * vh
             u[:] = ev + ds * self.P12 * bh
-            self.t_rho.copy_(torch.from_numpy(np.fft.ifft(ev + ds * self.P1 * bh, axis=1)))
+            self._put_t(np.fft.ifft(ev + ds * self.P1 * bh, axis=1))
             return
         elif mode == 1:
             new = u + ds * self.P2 * bh
         else:
             new = self.E * vh + ds * self.P1 * bh
         vh[:] = new
-        self.t_rho.copy_(torch.from_numpy(np.fft.ifft(new, axis=1)))
+        self._put_t(np.fft.ifft(new, axis=1))
 
     def red_values(self):
         return self.red.numpy().view(np.float64)
