@@ -281,6 +281,9 @@ struct nwb_plan {
   int rho_next_pf = 0;       // L2 prefetch of column k + rho_next_pf's input (NWB_RHO_NEXTPF)
   int rho_roll = 0;          // combine: L2 prefetch of the operands rho_roll rounds ahead (NWB_RHO_ROLL)
   int rho_debug = 0;
+  int rho_stagger_ns = 0, rho_stagger_mode = 0;  // NWB_RHO_STAGGER=<ns>[,<mode>]
+  int rho_bulk = 0;          // fp64 column load / store by TMA bulk copies (NWB_RHO_BULK)
+  int theta_bulk = 0;        // fp64 r2c row loads by TMA bulk copies (NWB_THETA_BULK)
   int theta_debug = 0;       // NWB_THETA_DEBUG (never set in production)         // NWB_RHO_DEBUG measurement knobs (never set in production)
   int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
   int rho_ws = 0, rho_ws2 = 0, rho_ws_ctas = 0;  // warp-specialised rho pass (k_rho_ws) group sizes, CTAs
@@ -386,6 +389,7 @@ template <typename T> ThetaArgs<T> theta_args(const nwb_plan* p) {
   a.msub = p->msub;
   a.tw_first = (const cplx<T>*)p->tw_first;
   a.ilv = p->ilv;
+  a.bulk = p->theta_bulk;
   return a;
 }
 
@@ -412,6 +416,15 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.ws_threads2 = p->rho_ws2;
   a.ws_ctas = p->rho_ws_ctas;
   a.roll = p->rho_roll;
+  a.bulk = p->rho_bulk;
+  a.stagger_ns = p->rho_stagger_ns;
+  a.stagger_mode = p->rho_stagger_mode;
+  {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    a.stagger_slots = sms > 0 ? sms : 148;
+  }
   if (const char* env = std::getenv("NWB_RHO_WS_DEBUG")) a.ws_debug = std::atoi(env);
   a.scratch = (cplx<T>*)p->ws_scratch;
   a.dh2 = p->dh2;
@@ -1670,6 +1683,13 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     if (const char* env = std::getenv("NWB_RHO_NEXTPF")) p->rho_next_pf = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_ROLL")) p->rho_roll = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_DEBUG")) p->rho_debug = std::atoi(env);
+    if (const char* env = std::getenv("NWB_RHO_STAGGER"))
+      std::sscanf(env, "%d,%d", &p->rho_stagger_ns, &p->rho_stagger_mode);
+    // 16-byte elements keep every padded chunk 16-byte aligned in shared memory
+    p->rho_bulk = precision == NWB_F64 ? 1 : 0;
+    if (const char* env = std::getenv("NWB_RHO_BULK")) p->rho_bulk = p->rho_bulk && env[0] != '0';
+    p->theta_bulk = precision == NWB_F64 ? 1 : 0;
+    if (const char* env = std::getenv("NWB_THETA_BULK")) p->theta_bulk = p->theta_bulk && env[0] != '0';
     if (const char* env = std::getenv("NWB_THETA_DEBUG")) p->theta_debug = std::atoi(env);
     if (const char* env = std::getenv("NWB_RHO_PERSIST")) p->rho_persistent = env[0] == '1';
     if (p->rho_debug) p->rho_persistent = 0;  // the knobs live in k_rho
@@ -1763,6 +1783,13 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     // and the combine prefetches each round's operand rows one round ahead
     // (fp64 rho 1.060 -> 1.034 ms per step, fp32 0.601 -> 0.582)
     if (!std::getenv("NWB_RHO_ROLL")) p->rho_roll = 1;
+    // One column per SM: all SMs would load, transform and stream in lockstep,
+    // so HBM idles during the transforms.  The first wave's CTAs start
+    // staggered over about one column period (40 us at C2 fp64, 30 us fp32) so
+    // some SMs stream while others transform (tools/rho_probe.py, C2: fp64
+    // rho 1.041 -> 1.014 ms per step, fp32 0.582 -> 0.574; larger spreads
+    // measured slower).
+    if (!std::getenv("NWB_RHO_STAGGER")) p->rho_stagger_ns = p->rsz == 8 ? 40000 : 30000;
   }
   if (e == cudaSuccess && p->rho_ws > 0) {
     int sms = 0;

@@ -24,8 +24,6 @@
 namespace nwb {
 
 #define NWB_MAX_PASSES 16
-#define NWB_FFT_PRAGMA_(x) _Pragma(#x)
-#define NWB_FFT_PRAGMA(x) NWB_FFT_PRAGMA_(x)
 
 struct FftDesc {
   int n;
@@ -261,9 +259,6 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
   const int total = per_row * rows;
   const V* twa = tw + d.pofs_a[p];
   const V* fia = tw + d.pfin_a[p];
-#ifdef NWB_PASS_UNROLL
-  NWB_FFT_PRAGMA(unroll NWB_PASS_UNROLL)
-#endif
   for (int g = tid; g < total; g += nth) {
     const int row = (int)fdiv((unsigned)g, d.pmag_row[p]);
     const int h = g - row * per_row;

@@ -60,6 +60,7 @@ template <typename T> struct ThetaArgs {
   int r1, msub;
   const cplx<T>* tw_first;
   int ilv;                    // transit layout: 1 = position q msub + i stored at i r1 + q
+  int bulk;                   // r2c row loads as TMA bulk copies (fp64 rows)
 };
 
 template <typename T> struct RhoArgs {
@@ -89,6 +90,12 @@ template <typename T> struct RhoArgs {
   int next_pf;                // > 0: prefetch the input column k + next_pf into L2 after the combine
   int roll;                   // > 0: the combine prefetches its operands roll rounds ahead into L2
   int debug;                  // measurement knobs (NWB_RHO_DEBUG): 1 skip FFTs, 2 skip combine loads
+  // phase stagger of the first wave (one column per SM): CTA slot s of the
+  // first `stagger_slots` blocks sleeps (s mod stagger_slots) * stagger_ns /
+  // stagger_slots before starting (stagger_mode 1: odd slots sleep stagger_ns),
+  // so SMs stream while others transform instead of all streaming at once
+  int stagger_ns, stagger_slots, stagger_mode;
+  int bulk;                   // column load / store as TMA bulk copies (fp64 columns)
   int persistent;             // march modes run k_rho_stream (one CTA per SM walking columns)
   // warp-specialised pass (k_rho_ws): transform / combine group sizes (0 = off),
   // CTAs (<= SMs x CTAs per SM) and their scratch (2 rows of ld per CTA)

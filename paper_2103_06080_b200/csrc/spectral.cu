@@ -48,14 +48,7 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 #ifndef NWB_THETA_MINB64
 #define NWB_THETA_MINB64 2
 #endif
-// unroll of the theta pre / post loops (independent iterations: several
-// table loads and shared-memory gathers in flight per thread)
-#ifndef NWB_POST_UNROLL
-#define NWB_POST_UNROLL 1
-#endif
-#define NWB_PRAGMA_(x) _Pragma(#x)
-#define NWB_PRAGMA(x) NWB_PRAGMA_(x)
-#define NWB_UNROLL(n) NWB_PRAGMA(unroll n)
+
 #ifndef NWB_RHO_THREADS_LB
 #define NWB_RHO_THREADS_LB 512
 #endif
@@ -104,7 +97,6 @@ __device__ __forceinline__ void c2r_pre(cplx<T>* z, const ThetaArgs<T>& a, int r
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     V* zr = z + r * rs;
-    NWB_UNROLL(NWB_POST_UNROLL)
     for (int k = threadIdx.x; k < npairs; k += blockDim.x) {
       const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
       V xk = zr[sk];
@@ -136,7 +128,6 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
     V* drow = reinterpret_cast<V*>(dst + (size_t)j * a.g.nt);
     T hi = -INFINITY, lo = INFINITY;
     bool nan = false;
-    NWB_UNROLL(NWB_POST_UNROLL)
     for (int n = threadIdx.x; n < m; n += blockDim.x) {
       const V zz = zr[pidx(a.dh, __ldg(&a.pos_h[n]))];
       const T v0 = zz.x * scale, v1 = zz.y * scale;
@@ -235,7 +226,6 @@ __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
-  NWB_UNROLL(NWB_POST_UNROLL)
   for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
     const int r = idx % R, k = idx / R, j = j0 + r;
     if (j >= jend) continue;
@@ -311,18 +301,44 @@ __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R, SP
   const int jstep = SPLIT ? a.msub : 1;
   const T* src = a.phys_in + (size_t)mem * nr * a.g.nt;
   const int rs = padded_len(m, a.dh.pad_period);
+  if (a.bulk && !(a.debug & 4)) {
+    // rows as bulk copies of the padded line's P-element chunks (TMA engine)
+    __shared__ __align__(8) unsigned long long bar;
+    const int P = a.dh.pad_period ? a.dh.pad_period : 256;
+    const int nch = (m + P - 1) / P;
+    int valid = 0;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int j = j0 + r * jstep;
-    V* zr = z + r * rs;
-    const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
-    for (int n = threadIdx.x; n < m && !(a.debug & 4); n += blockDim.x) {
-      if (j < jend) cp_async_c(&zr[pidx(a.dh, n)], &srow[n]);
-      else zr[pidx(a.dh, n)] = mk<V>(0, 0);
+    for (int r = 0; r < R; ++r) valid += j0 + r * jstep < jend;
+    if (threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) mbar_arrive_expect_tx(&bar, (unsigned)(valid * m * sizeof(V)));
+    for (int idx = threadIdx.x; idx < nch * R; idx += blockDim.x) {
+      const int r = idx / nch, c = idx - r * nch, j = j0 + r * jstep;
+      const int e0 = c * P, cnt = min(P, m - e0);
+      V* zr = z + r * rs;
+      if (j < jend) {
+        const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
+        bulk_g2s(&zr[pidx(a.dh, e0)], srow + e0, (unsigned)(cnt * sizeof(V)), &bar);
+      } else {
+        for (int e = e0; e < e0 + cnt; ++e) zr[pidx(a.dh, e)] = mk<V>(0, 0);
+      }
     }
+    mbar_wait(&bar, 0);
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int j = j0 + r * jstep;
+      V* zr = z + r * rs;
+      const V* srow = reinterpret_cast<const V*>(src + (size_t)j * a.g.nt);
+      for (int n = threadIdx.x; n < m && !(a.debug & 4); n += blockDim.x) {
+        if (j < jend) cp_async_c(&zr[pidx(a.dh, n)], &srow[n]);
+        else zr[pidx(a.dh, n)] = mk<V>(0, 0);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
   }
-  cp_async_wait_all();
-  __syncthreads();
   fft_forward(z, a.dh, R, rs, a.tw_h);
   if (a.debug & 4) return;
   if (SPLIT) r2c_post_split<T, R>(z, a, rs, mem, j0);
@@ -529,10 +545,41 @@ __device__ __forceinline__ size_t rho_io(const RhoArgs<T>& a, size_t row, int k,
   return (size_t)a.g.kk * st + (size_t)k * len + (j - st);
 }
 
+// The column's padded shared-memory line is contiguous between pad slots,
+// so a column moves as ceil(n / P) bulk copies of P elements (TMA engine,
+// one mbarrier for the load) instead of n per-element cp.async.
+template <typename V>
+__device__ __forceinline__ void column_bulk_load(V* x, const FftDesc& d, const V* src, int n,
+                                                 unsigned long long* bar) {
+  const int P = d.pad_period ? d.pad_period : 256;
+  const int nch = (n + P - 1) / P;
+  if (threadIdx.x == 0) mbar_init(bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive_expect_tx(bar, (unsigned)(n * sizeof(V)));
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    const int e0 = c * P, cnt = min(P, n - e0);
+    bulk_g2s(&x[pidx(d, e0)], src + e0, (unsigned)(cnt * sizeof(V)), bar);
+  }
+  mbar_wait(bar, 0);
+}
+template <typename V>
+__device__ __forceinline__ void column_bulk_store(V* dst, const FftDesc& d, const V* x, int n) {
+  const int P = d.pad_period ? d.pad_period : 256;
+  const int nch = (n + P - 1) / P;
+  fence_proxy_async_smem();
+  __syncthreads();
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    const int e0 = c * P, cnt = min(P, n - e0);
+    bulk_s2g(dst + e0, &x[pidx(d, e0)], (unsigned)(cnt * sizeof(V)));
+  }
+  bulk_commit_wait_read();
+}
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho(const RhoArgs<T> a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long load_bar;
   V* x = reinterpret_cast<V*>(smem_raw);
   const int n = a.dr.n;
   const int mem = blockIdx.x, k = blockIdx.y;
@@ -543,6 +590,22 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
     V* dst = a.out + row;
     for (int f = threadIdx.x; f < n; f += blockDim.x) dst[f] = src[a.pos_r[f]];
     return;
+  }
+  if (a.stagger_ns > 0) {
+    const int slot = blockIdx.x + blockIdx.y * gridDim.x;  // linear block id
+    if (slot < a.stagger_slots) {
+      const long long wait = a.stagger_mode == 1 ? ((slot & 1) ? a.stagger_ns : 0)
+                                                 : (long long)slot * a.stagger_ns / a.stagger_slots;
+      if (threadIdx.x == 0 && wait > 0) {
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+          __nanosleep(500);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while ((long long)(t - t0) < wait);
+      }
+      __syncthreads();
+    }
   }
   if (a.prefetch && threadIdx.x == 0) {
     // the combine operands are consumed after the forward FFT: start their
@@ -573,6 +636,8 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   } else if (a.blk_n) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &a.in[rho_io(a, row, k, j)]);
     cp_async_wait_all();
+  } else if (a.bulk && !(a.debug & 4)) {
+    column_bulk_load(x, a.dr, src, n, &load_bar);
   } else if (!(a.debug & 4)) {
     for (int j = threadIdx.x; j < n; j += blockDim.x) cp_async_c(&x[pidx(a.dr, j)], &src[j]);
     cp_async_wait_all();
@@ -597,6 +662,8 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   V* dst = a.out + row;
   if (a.blk_n)
     for (int j = threadIdx.x; j < n; j += blockDim.x) a.out[rho_io(a, row, k, j)] = x[pidx(a.dr, j)];
+  else if (a.bulk && !(a.debug & 4))
+    column_bulk_store(dst, a.dr, x, n);
   else if (!(a.debug & 4))
     for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;

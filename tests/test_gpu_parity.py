@@ -500,3 +500,22 @@ def test_large_host_load_staged_equals_device_load(cuda, precision):
         outs.append(out.cpu().numpy())
         plan.close()
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("shape", [(10000, 3584), (1250, 448), (8192, 16384)])
+def test_transforms_vs_cufft(cuda, shape):
+    """Cross-check against cuFFT (torch.fft, library code used only here as a
+    second opinion beside scipy): rfft2 / irfft2 of the C2, Set-1 and C5 grids."""
+    import torch
+
+    g = torch.Generator(device=cuda).manual_seed(shape[0])
+    x = torch.randn(shape, dtype=torch.float64, device=cuda, generator=g)
+    tr = nw.SpectralTransforms(*shape)
+    ours = tr.forward(x)
+    ref = torch.fft.rfft2(x)
+    err = float((ours - ref).abs().max() / ref.abs().max())
+    assert err <= 1e-14, err
+    back = tr.inverse(ref)
+    ref_back = torch.fft.irfft2(ref, s=shape)
+    err = float((back - ref_back).abs().max() / ref_back.abs().max())
+    assert err <= 1e-14, err
