@@ -246,16 +246,21 @@ class SlabMarch:
     GUARD_EVERY = 16
 
     def __init__(self, config: DomainConfig, fields, precision: str = "double", group=None,
-                 ops=None, device=None, max_steps: int | None = None):
+                 ops=None, device=None, max_steps: int | None = None, comm=None):
+        """``comm``: an object with ``geo`` (SlabGeometry) and the ``exchange`` /
+        ``max_`` / ``halo`` collectives, replacing torch.distributed (the GPU tests
+        drive several virtual ranks in one process through host barriers)."""
         import torch
 
         self.cfg = config
-        if group is not None or _dist().is_available() and _dist().is_initialized():
+        if comm is not None:
+            world, rank = comm.geo.world, comm.geo.rank
+        elif group is not None or _dist().is_available() and _dist().is_initialized():
             world, rank = _dist().get_world_size(group), _dist().get_rank(group)
         else:
             world, rank = 1, 0
         self.geo = SlabGeometry(config.N_rho, config.N_theta, world, rank)
-        self.comm = _Comm(group, self.geo)
+        self.comm = comm if comm is not None else _Comm(group, self.geo)
         self.ops = ops or GpuSlabOps(config, self.geo, precision, device)
         self.n_steps = config.N_sigma if max_steps is None else min(config.N_sigma, max_steps)
         self.ops.set_coeffs(fields, self.n_steps + 1)

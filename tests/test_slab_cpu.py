@@ -81,3 +81,27 @@ def test_slab_march_matches_single_process_oracle(tmp_path, world):
     ref = nwave_oracle.march(cfg, v0, fields)
     assert np.max(np.abs(field - ref.final)) <= 1e-13 * np.max(np.abs(ref.final))
     assert max(max_abs.max(), vmax) == pytest.approx(ref.max_abs_v, rel=1e-13)
+
+
+def test_block_major_transit_layout_roundtrip():
+    """The rho-side transit layout (slab.py): rank b's rows form one contiguous
+    (modes x rows_b) block at modes * start_b, i.e. exactly all_to_all_single's
+    rank-ordered segments; natural <-> block-major is a bijection."""
+    import torch
+
+    from paper_2103_06080_b200.slab import (SlabGeometry, blocks_to_natural, natural_to_blocks,
+                                            rank_row_starts)
+
+    for n_rho, world in ((24, 1), (24, 3), (10, 4), (7, 2)):
+        starts = rank_row_starts(n_rho, world)
+        assert starts[0] == 0 and starts[-1] == n_rho and all(a <= b for a, b in zip(starts, starts[1:]))
+        modes = 5
+        nat = torch.arange(modes * n_rho, dtype=torch.float64).reshape(modes, n_rho)
+        flat = torch.empty(modes * n_rho, dtype=torch.float64)
+        natural_to_blocks(nat, flat, starts)
+        for b in range(world):
+            a, e = starts[b], starts[b + 1]
+            assert torch.equal(flat[modes * a:modes * e].reshape(modes, e - a), nat[:, a:e])
+        assert torch.equal(blocks_to_natural(flat, modes, starts), nat)
+        geo = SlabGeometry(n_rho, 16, world, 0)
+        assert starts[:-1] == [geo.rows(r).start for r in range(world)]
