@@ -169,6 +169,11 @@ int nwb_slab_weno(nwb_slab* slab, const void* v_ext_dev, void* b_dev, int sigma_
 int nwb_slab_theta_r2c(nwb_slab* slab, const void* b_dev, void* spec_rows_dev);
 int nwb_slab_rho(nwb_slab* slab, int mode, const void* bt_dev, void* out_dev, void* vh_dev,
                  void* u_dev);
+/* nwb_slab_rho over the local theta modes [k_begin, k_end) only: the slab
+ * march runs the rho pass in mode chunks so each chunk's all-to-all overlaps
+ * the next chunk's transforms. */
+int nwb_slab_rho_range(nwb_slab* slab, int mode, int k_begin, int k_end, const void* bt_dev,
+                       void* out_dev, void* vh_dev, void* u_dev);
 
 /* Standalone multiplier tables in natural (n_rho, n_theta/2+1) layout; any
  * output may be NULL.  z is always complex128. */

@@ -37,7 +37,8 @@ ABI_SYMBOLS = (
     "nwb_weno5_b", "nwb_tables", "nwb_phi", "nwb_combine", "nwb_profile_kernels",
     "nwb_turbulence_fields", "nwb_slab_create", "nwb_slab_destroy", "nwb_slab_set_stream",
     "nwb_slab_layout", "nwb_slab_set_coeffs", "nwb_slab_theta_c2r", "nwb_slab_weno",
-    "nwb_slab_theta_r2c", "nwb_slab_rho", "nwb_slab_set_blocks", "nwb_ground_metrics",
+    "nwb_slab_theta_r2c", "nwb_slab_rho", "nwb_slab_set_blocks", "nwb_slab_rho_range",
+    "nwb_ground_metrics",
     "nwb_split_create",
     "nwb_split_destroy", "nwb_split_set_stream", "nwb_split_set_coeffs", "nwb_split_load",
     "nwb_split_store", "nwb_split_stage", "nwb_split_march", "nwb_godunov_flux",
@@ -90,6 +91,8 @@ def _declare(lib):
         "nwb_slab_set_stream": (c_int, [c_void_p, c_void_p]),
         "nwb_slab_layout": (c_int, [c_void_p, P(c_int), P(c_int)]),
         "nwb_slab_set_blocks": (c_int, [c_void_p, c_int, c_void_p]),
+        "nwb_slab_rho_range": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                       c_void_p]),
         "nwb_slab_set_coeffs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                         c_int]),
         "nwb_slab_theta_c2r": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p]),

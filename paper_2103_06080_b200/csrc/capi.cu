@@ -1289,7 +1289,7 @@ template <typename T> int slab_r2c_impl(nwb_slab* s, const void* b, void* spec) 
 }
 
 template <typename T> int slab_rho_impl(nwb_slab* s, int mode, const void* bt, void* out, void* vh,
-                                        void* u) {
+                                        void* u, int k0 = 0, int k1 = -1) {
   RhoArgs<T> q{};
   q.g = Geom{s->nr, s->nt, s->m, s->modes, s->ld_rho, 1};
   q.dr = s->dr;
@@ -1307,6 +1307,9 @@ template <typename T> int slab_rho_impl(nwb_slab* s, int mode, const void* bt, v
   q.prefetch = 100;
   q.blk_n = s->blk_n;
   for (int b = 0; b <= s->blk_n && b < 17; ++b) q.blk_start[b] = s->blk_start[b];
+  q.k_off = k0;
+  q.k_cnt = (k1 < 0 ? s->modes : k1) - k0;
+  if (q.k_cnt <= 0) return NWB_OK;
   launch_rho<T>(q, mode, s->rho_threads, s->stream);
   CHECK_LAUNCH("slab rho");
   return NWB_OK;
@@ -1621,6 +1624,15 @@ int nwb_slab_rho(nwb_slab* s, int mode, const void* bt, void* out, void* vh, voi
   if (mode < RHO_STAGE1 || mode > RHO_INIT) return fail(NWB_EINVAL, "unknown rho mode");
   return s->prec == NWB_F64 ? slab_rho_impl<double>(s, mode, bt, out, vh, u)
                             : slab_rho_impl<float>(s, mode, bt, out, vh, u);
+}
+
+int nwb_slab_rho_range(nwb_slab* s, int mode, int k_begin, int k_end, const void* bt, void* out,
+                       void* vh, void* u) {
+  if (!s) return fail(NWB_EINVAL, "null slab");
+  if (mode < RHO_STAGE1 || mode > RHO_INIT) return fail(NWB_EINVAL, "unknown rho mode");
+  if (k_begin < 0 || k_end > s->modes || k_begin > k_end) return fail(NWB_EINVAL, "mode range outside the slab");
+  return s->prec == NWB_F64 ? slab_rho_impl<double>(s, mode, bt, out, vh, u, k_begin, k_end)
+                            : slab_rho_impl<float>(s, mode, bt, out, vh, u, k_begin, k_end);
 }
 
 int nwb_profile_kernels(nwb_plan* p, int scheme, int n0, int n_steps, float* kernel_ms) {

@@ -115,6 +115,7 @@ template <typename T> struct RhoArgs {
   // all-to-all's segments, so it moves them without packing copies
   int blk_n;
   int blk_start[17];
+  int k_off, k_cnt;           // theta modes [k_off, k_off + k_cnt) of the launch (k_cnt 0: to kk): slab chunks
   int r1, ilv;
   FftDesc dsub;
   const cplx<T>* tw_sub;

@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   __shared__ __align__(8) unsigned long long load_bar;
   V* x = reinterpret_cast<V*>(smem_raw);
   const int n = a.dr.n;
-  const int mem = blockIdx.x, k = blockIdx.y;
+  const int mem = blockIdx.x, k = blockIdx.y + a.k_off;
   const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
   const size_t trow = (size_t)k * a.g.ld;
   const V* src = a.in + row;
@@ -1159,7 +1159,7 @@ static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
   }
   const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);
   cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  dim3 grid(a.g.batch, a.g.kk);
+  dim3 grid(a.g.batch, a.k_cnt > 0 ? a.k_cnt : a.g.kk - a.k_off);
   k_rho<T, MODE><<<grid, threads, sm, s>>>(a);
   }
 }

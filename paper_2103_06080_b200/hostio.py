@@ -102,9 +102,10 @@ class SnapshotStreamer:
         self.copy_stream = torch.cuda.Stream(device=plan.device)
         self.results: dict = {}
         self.errors: list = []
+        self._threads: list = []
         self._n = 0
 
-    def capture(self, key, shape=None):
+    def capture(self, key):
         """Snapshot the plan's current state (v at the start of the next step)."""
         torch = _torch()
         k = self._n & 1
@@ -122,7 +123,7 @@ class SnapshotStreamer:
         self.free[k].clear()
         th = threading.Thread(target=self._drain, args=(k, slot, ready, key), daemon=True)
         th.start()
-        self._threads = getattr(self, "_threads", []) + [th]
+        self._threads.append(th)
 
     def _drain(self, k, slot, ready, key):
         torch = _torch()
@@ -138,7 +139,7 @@ class SnapshotStreamer:
             self.free[k].set()
 
     def finish(self) -> dict:
-        for th in getattr(self, "_threads", []):
+        for th in self._threads:
             th.join()
         if self.errors:
             raise self.errors[0]

@@ -4,7 +4,7 @@ Rank r owns rho rows ``rows_r`` on the physical / theta side (theta c2r,
 WENO, theta r2c act on whole rows) and theta modes ``modes_r`` on the rho side
 (the rho passes transform whole columns).  Per ExpRK22 stage:
 
-    rho pass (own modes)  --all-to-all-->  theta c2r (own rows)
+    rho pass (own modes, in chunks)  --point-to-point per chunk-->  theta c2r (own rows)
       -> all-reduce MAX of [alpha_theta, max|V|]   (alpha must be global, weno.py:114)
       -> 3-row halo exchange with the ring neighbours (periodic rho)
       -> WENO -> theta r2c  --all-to-all-->  next rho pass
@@ -27,8 +27,14 @@ rho-side ``bt_rho`` / ``t_rho`` are block-major -- the block of rank b's rows
 (my modes x rows_b) is contiguous at modes * row_start_b (``nwb_slab_set_blocks``;
 the rho kernels read and write that layout).  Both sides are then exactly
 ``all_to_all_single``'s rank-ordered segments: no packing or unpacking
-copies.  The divergence guard is kept on the device (a per-step history of
-the all-reduced max|V|) and checked on the host every ``GUARD_EVERY`` steps.
+copies.  The rho pass runs in mode chunks (``chunks``, 4 by default on
+several ranks): each chunk's blocks leave by point-to-point sends right after
+its transforms (on the process group's stream) while the next chunk
+transforms, so that transpose overlaps compute; the theta -> rho transpose
+is one in-place all_to_all_single (a row chunk of the theta-side spectrum is
+not contiguous).  The divergence guard is kept on the device (a per-step
+history of the all-reduced max|V|) and checked on the host every
+``GUARD_EVERY`` steps.
 """
 
 from __future__ import annotations
@@ -112,6 +118,27 @@ class _Comm:
         f = 2 if real else 1
         _dist().all_to_all_single(o, i, [f * n for n in out_splits], [f * n for n in in_splits],
                                   group=self.group)
+
+    def sendrecv_async(self, sends, recvs):
+        """Point-to-point sends [(dst, tensor)] and receives [(src, tensor)],
+        issued after the work queued on the current stream; returns handles
+        for ``wait``.  The NCCL kernels run on the process group's stream, so
+        kernels queued on other streams afterwards overlap them."""
+        import torch
+
+        dist = _dist()
+        ops = []
+        for dst, t in sends:
+            ops.append(dist.P2POp(dist.isend, torch.view_as_real(t) if torch.is_complex(t) else t,
+                                  dst, self.group))
+        for src, t in recvs:
+            ops.append(dist.P2POp(dist.irecv, torch.view_as_real(t) if torch.is_complex(t) else t,
+                                  src, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def wait(self, handles):
+        for h in handles:
+            h.wait()
 
     def max_(self, t):
         if self.geo.world > 1:
@@ -229,9 +256,12 @@ class GpuSlabOps:
         self._run(self.lib.nwb_slab_theta_r2c, (self.b if src is None else src).data_ptr(),
                   self.spec_rows.data_ptr())
 
-    def rho(self, mode: int):
-        self._run(self.lib.nwb_slab_rho, mode, self.bt_rho.data_ptr(), self.t_rho.data_ptr(),
-                  self.vh.data_ptr(), self.u.data_ptr())
+    def rho(self, mode: int, k0: int = 0, k1: int | None = None, out=None):
+        """rho pass over local modes [k0, k1) into ``out`` (default t_rho)."""
+        k1 = len(self.geo.modes()) if k1 is None else k1
+        dst = self.t_rho if out is None else out
+        self._run(self.lib.nwb_slab_rho_range, mode, k0, k1, self.bt_rho.data_ptr(),
+                  dst.data_ptr(), self.vh.data_ptr(), self.u.data_ptr())
 
     def red_values(self):
         return self.red.cpu().numpy().view(np.float64)
@@ -246,7 +276,8 @@ class SlabMarch:
     GUARD_EVERY = 16
 
     def __init__(self, config: DomainConfig, fields, precision: str = "double", group=None,
-                 ops=None, device=None, max_steps: int | None = None, comm=None):
+                 ops=None, device=None, max_steps: int | None = None, comm=None,
+                 chunks: int | None = None):
         """``comm``: an object with ``geo`` (SlabGeometry) and the ``exchange`` /
         ``max_`` / ``halo`` collectives, replacing torch.distributed (the GPU tests
         drive several virtual ranks in one process through host barriers)."""
@@ -271,15 +302,50 @@ class SlabMarch:
         g = self.geo
         rows_me, modes_me = len(g.rows()), len(g.modes())
         # all-to-all segment sizes (complex elements), rank order
-        self._r2t_in = [modes_me * len(g.rows(s)) for s in range(g.world)]
-        self._r2t_out = [len(g.modes(r)) * rows_me for r in range(g.world)]
         self._t2r_in = [len(g.modes(s)) * rows_me for s in range(g.world)]
         self._t2r_out = [modes_me * len(g.rows(r)) for r in range(g.world)]
+        # the rho pass runs in mode chunks; chunk c's rho -> theta exchange
+        # (point-to-point, in place) overlaps chunk c+1's transforms
+        self.chunks = max(1, chunks if chunks is not None else (4 if g.world > 1 else 1))
+        self._starts = rank_row_starts(g.n_rho, g.world)
+
+    @staticmethod
+    def _chunk(n: int, chunks: int, c: int):
+        return (n * c) // chunks, (n * (c + 1)) // chunks
 
     # -- layout changes (in place: see the module docstring) ----------------
-    def _rho_to_theta(self):
-        o = self.ops
-        self.comm.exchange(o.spec_rows.reshape(-1), o.t_rho.reshape(-1), self._r2t_out, self._r2t_in)
+    def _rho_exchange(self, mode: int):
+        """rho pass + rho -> theta exchange.  One rank: the rho pass writes
+        the theta-side spectrum directly (the layouts coincide).  Several: mode
+        chunks, each chunk's blocks sent point to point right after its
+        transforms while the next chunk transforms."""
+        g, o = self.geo, self.ops
+        if g.world == 1:
+            o.rho(mode, out=o.spec_rows.reshape(-1))
+            return
+        me, rows_me, modes_me = g.rank, len(g.rows()), len(g.modes())
+        t_flat, s_rows = o.t_rho.reshape(-1), o.spec_rows
+        pending = []
+        for c in range(self.chunks):
+            a, b = self._chunk(modes_me, self.chunks, c)
+            if b > a:
+                o.rho(mode, a, b)
+            sends, recvs = [], []
+            for r in range(g.world):
+                st, ln = self._starts[r], self._starts[r + 1] - self._starts[r]
+                if b > a and ln > 0:  # my chunk of rank r's row block
+                    seg = t_flat[modes_me * st + a * ln:modes_me * st + b * ln]
+                    if r == me:
+                        s_rows[g.modes().start + a:g.modes().start + b].reshape(-1).copy_(seg)
+                    else:
+                        sends.append((r, seg))
+                mr = g.modes(r)
+                ar, br = self._chunk(len(mr), self.chunks, c)
+                if r != me and br > ar and rows_me > 0:
+                    recvs.append((r, s_rows[mr.start + ar:mr.start + br].reshape(-1)))
+            pending.append(self.comm.sendrecv_async(sends, recvs))
+        for h in pending:
+            self.comm.wait(h)
 
     def _theta_to_rho(self):
         o = self.ops
@@ -295,11 +361,10 @@ class SlabMarch:
             if not isinstance(v0_rows, torch.Tensor) else v0_rows.to(o.b.device, o.b.dtype)
         o.r2c(src)
         self._theta_to_rho()
-        o.rho(RHO_INIT)
+        self._rho_exchange(RHO_INIT)
 
     def _stage(self, row: int, mode: int, guard_step: int | None):
         o = self.ops
-        self._rho_to_theta()
         o.red.zero_()
         o.c2r(row, reduce=True)
         self.comm.max_(o.red)
@@ -309,7 +374,7 @@ class SlabMarch:
         o.weno(row)
         o.r2c()
         self._theta_to_rho()
-        o.rho(mode)
+        self._rho_exchange(mode)
 
     def _check_guard(self, upto: int, guard: float):
         """Host check of the guard history for steps [checked, upto)."""
@@ -343,7 +408,6 @@ class SlabMarch:
     def final_rows(self):
         """This rank's rows of V at the end of the march, and the global max|V|."""
         o = self.ops
-        self._rho_to_theta()
         o.red.zero_()
         o.c2r(self.n_steps, reduce=True)
         self.comm.max_(o.red)

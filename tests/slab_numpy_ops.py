@@ -72,28 +72,36 @@ class NumpySlabOps:
         x = (self.b if src is None else src).numpy()
         self.spec_rows.copy_(torch.from_numpy(np.fft.rfft(x, axis=1).T.copy()))
 
-    def _put_t(self, nat):
-        natural_to_blocks(torch.from_numpy(np.ascontiguousarray(nat)), self.t_rho, self.starts)
-
-    def rho(self, mode):
+    def rho(self, mode, k0=0, k1=None, out=None):
+        """Modes [k0, k1) of the rho pass into ``out`` (default t_rho), both in
+        the block-major transit layout (one block = natural (modes, n_rho))."""
         nmodes = len(self.geo.modes())
-        bt = blocks_to_natural(self.bt_rho, nmodes, self.starts).numpy()
+        k1 = nmodes if k1 is None else k1
+        sl = slice(k0, k1)
+        bt = blocks_to_natural(self.bt_rho, nmodes, self.starts).numpy()[sl]
         bh = np.fft.fft(bt, axis=1)
         ds = self.cfg.d_sigma
-        vh, u = self.vh.numpy(), self.u.numpy()
+        vh, u = self.vh.numpy()[sl], self.u.numpy()[sl]
+        E, P1, P12, P2 = self.E[sl], self.P1[sl], self.P12[sl], self.P2[sl]
         if mode == 3:
             new = bh
         elif mode == 0:
-            ev = self.E * vh
-            u[:] = ev + ds * self.P12 * bh
-            self._put_t(np.fft.ifft(ev + ds * self.P1 * bh, axis=1))
-            return
+            ev = E * vh
+            u[:] = ev + ds * P12 * bh
+            new = None
+            res = np.fft.ifft(ev + ds * P1 * bh, axis=1)
         elif mode == 1:
-            new = u + ds * self.P2 * bh
+            new = u + ds * P2 * bh
         else:
-            new = self.E * vh + ds * self.P1 * bh
-        vh[:] = new
-        self._put_t(np.fft.ifft(new, axis=1))
+            new = E * vh + ds * P1 * bh
+        if new is not None:
+            vh[:] = new
+            res = np.fft.ifft(new, axis=1)
+        dst = self.t_rho if out is None else out
+        chunk = torch.from_numpy(np.ascontiguousarray(res))
+        for b in range(len(self.starts) - 1):
+            a, e = self.starts[b], self.starts[b + 1]
+            dst[nmodes * a + k0 * (e - a):nmodes * a + k1 * (e - a)] = chunk[:, a:e].reshape(-1)
 
     def red_values(self):
         return self.red.numpy().view(np.float64)

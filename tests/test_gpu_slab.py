@@ -75,6 +75,20 @@ class _ThreadComm:
             o += n
         self._sync()
 
+    def sendrecv_async(self, sends, recvs):
+        r = self.geo.rank
+        self._sync()
+        for dst, t in sends:
+            self.shared[(r, dst)] = t
+        self._sync()
+        for src, t in recvs:
+            t.copy_(self.shared[(src, r)])
+        self._sync()
+        return []
+
+    def wait(self, handles):
+        pass
+
     def max_(self, t):
         import torch
 
