@@ -1791,7 +1791,9 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     const int per_sm = (int)(smem_max / ((size_t)n_rho * csz * 9 / 8));
-    if (!std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = p->rsz == 8 ? 40 : 25;
+    // (fp64 re-tuned with the first-wave stagger and bulk column loads: 40 % -> 20 %,
+    // rho 1.010 -> 0.994 ms per step)
+    if (!std::getenv("NWB_RHO_PREFETCH")) p->rho_prefetch = p->rsz == 8 ? 20 : 25;
     if (!std::getenv("NWB_RHO_NEXTPF")) p->rho_next_pf = sms * (per_sm < 1 ? 1 : per_sm);
     // and the combine prefetches each round's operand rows one round ahead
     // (fp64 rho 1.060 -> 1.034 ms per step, fp32 0.601 -> 0.582)
