@@ -459,8 +459,18 @@ template <typename T> WenoArgs<T> weno_args(const nwb_plan* p) {
 constexpr int EV_PER_STAGE = 5;
 
 inline void rec_event(const nwb_plan* p, cudaEvent_t e, cudaStream_t s) {
+  if (!e) return;  // the timed graph records only the bucket boundaries it needs
   if (p->ev_external) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
   else cudaEventRecord(e, s);
+}
+
+// Events the timed step graph records: step start, WENO start and r2c end of
+// each stage (the nonlinear bucket), step end.  The others (after WENO, after
+// the rho pass, stage-2 start) are not needed for the buckets, and every
+// event-record node costs a dependency break inside the graph.
+inline bool timed_event_needed(int i, int nev) {
+  const int in_stage = i % EV_PER_STAGE;
+  return i == 0 || i == nev - 1 || in_stage == 1 || in_stage == 3;
 }
 
 template <typename T>
@@ -880,10 +890,13 @@ template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
   p->tgraph_g[gi] = nullptr;
   for (auto& e : p->tev)
     if (!e) CU(cudaEventCreate(&e));
+  const int nev_all = (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1) * EV_PER_STAGE;
+  cudaEvent_t cap[10] = {};
+  for (int i = 0; i < nev_all; ++i) cap[i] = timed_event_needed(i, nev_all) ? p->tev[i] : nullptr;
   cudaGraph_t gr;
   CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   p->ev_external = true;
-  launch_step<T>(p, scheme, p->tev);
+  launch_step<T>(p, scheme, cap);
   p->ev_external = false;
   cudaError_t le = cudaGetLastError();
   CU(cudaStreamEndCapture(p->stream, &gr));
@@ -895,9 +908,12 @@ template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
   CU(cudaGraphGetNodes(gr, nullptr, &nn));
   std::vector<cudaGraphNode_t> nodes(nn);
   CU(cudaGraphGetNodes(gr, nodes.data(), &nn));
-  const int nev = (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1) * EV_PER_STAGE;
-  int found = 0;
-  for (int i = 0; i < nev; ++i) p->tnode[gi][i] = nullptr;
+  const int nev = nev_all;
+  int found = 0, want = 0;
+  for (int i = 0; i < nev; ++i) {
+    p->tnode[gi][i] = nullptr;
+    want += cap[i] != nullptr;
+  }
   for (auto nd : nodes) {
     cudaGraphNodeType ty;
     CU(cudaGraphNodeGetType(nd, &ty));
@@ -905,13 +921,13 @@ template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
     cudaEvent_t e;
     CU(cudaGraphEventRecordNodeGetEvent(nd, &e));
     for (int i = 0; i < nev; ++i)
-      if (p->tev[i] == e && !p->tnode[gi][i]) {
+      if (cap[i] && cap[i] == e && !p->tnode[gi][i]) {
         p->tnode[gi][i] = nd;
         ++found;
         break;
       }
   }
-  if (found != nev) {
+  if (found != want) {
     cudaGraphDestroy(gr);
     return fail(NWB_ECUDA, "timed graph: event-record nodes not found");
   }
@@ -954,7 +970,8 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
       cudaStreamSynchronize(p->stream);
       for (auto ex : p->tgraph[gi])
         if (ex)
-          for (int q = 0; q < nev; ++q) cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], p->tev[q]);
+          for (int q = 0; q < nev; ++q)
+            if (p->tnode[gi][q]) cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], p->tev[q]);
       cudaGetLastError();
     }
     for (auto& e : evs) cudaEventDestroy(e);
@@ -994,7 +1011,7 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
           e = cudaEventSynchronize(evs[(size_t)(st - nwb_plan::NTG) * 2 * EV_PER_STAGE + nev - 1]);
         int q = 0;
         for (; q < nev && e == cudaSuccess; ++q)
-          e = cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], ev[q]);
+          if (p->tnode[gi][q]) e = cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], ev[q]);
         const bool set_failed = e != cudaSuccess;
         if (e == cudaSuccess) e = cudaGraphLaunch(ex, p->stream);
         if (e != cudaSuccess) {
