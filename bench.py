@@ -185,7 +185,7 @@ KERNELS = ("theta_c2r", "weno", "theta_r2c", "rho_stage1", "theta_c2r", "weno", 
            "rho_stage2")
 
 
-def table_read_fraction(n: int) -> float:
+def table_read_fraction(n: int, pair55: bool = False) -> float:
     """Share of each multiplier-table row the rho combine reads: tables are
     read at the canonical +-f position (csrc/fft.cuh sym_pos), i.e. block 0 of
     the first-stage radix r1 plus half of the other blocks.  r1 restates the
@@ -198,6 +198,8 @@ def table_read_fraction(n: int) -> float:
             c[r] += 1
     c2 = c[2]
     c2 -= min(c[7], c2)                       # 7 pairs with 2
+    if pair55:                                 # fp32 plans: radix-25 passes first
+        c[5] %= 2
     for _ in range(c[5]):                      # 5 pairs with 3, else 2
         if c[3] > 0:
             c[3] -= 1
@@ -214,7 +216,8 @@ def table_read_fraction(n: int) -> float:
         else:
             c3 -= 1
     head = {1: 2, 2: 4, 3: 8}.get(c2 % 4)
-    r1 = head or (7 if c[7] else 5 if c[5] else 3 if c[3] else 4 if n % 4 == 0 else n)
+    r1 = head or (7 if c[7] else 5 if (c[5] or pair55 and n % 25 == 0) else 3 if c[3]
+                  else 4 if n % 4 == 0 else n)
     if r1 <= 1 or n % r1:
         return 1.0
     mm = n // r1
@@ -243,7 +246,8 @@ def algorithmic_bytes(cfg, precision: str, batch: int = 1, design: bool = False)
     r2c = batch * (phys + spec)
     rho1 = rho2 = batch * 4 * spec
     if design:
-        tf = table_read_fraction(cfg.N_rho)  # 0.6 at N_rho = 10000 (r1 = 5)
+        # 0.6 at N_rho = 10000 (r1 = 5); long fp32 columns use radix-25 passes (capi.cu)
+        tf = table_read_fraction(cfg.N_rho, precision == "single" and cfg.N_rho >= 5000)
         rho1 += int(3 * spec * tf)
         rho2 += int(spec * tf)
     return [c2r, weno, r2c, rho1, c2r, weno, r2c, rho2]

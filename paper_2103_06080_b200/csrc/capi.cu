@@ -52,7 +52,7 @@ struct FftPlanHost {
 
 // first > 1 forces a lone first stage of that radix (2, 3, 4, 5, 7): the
 // cluster-split rho pass (2) and the theta-fused first rho stage (r1).
-bool plan_fft(int n, int first, FftPlanHost& h, int max_prod = 16) {
+bool plan_fft(int n, int first, FftPlanHost& h, int max_prod = 16, int pair55 = 0) {
   int m = n, c2 = 0, c3 = 0, c5 = 0, c7 = 0;
   while (m % 2 == 0) { m /= 2; ++c2; }
   while (m % 3 == 0) { m /= 3; ++c3; }
@@ -72,6 +72,10 @@ bool plan_fft(int n, int first, FftPlanHost& h, int max_prod = 16) {
   for (; c7 > 0; --c7) {
     if (big && c2 > 0) { ps.push_back({7, 2}); --c2; } else ps.push_back({7, 1});
   }
+  // radix-25 passes (5.5) for the powers of 5 (pair55): one shared-memory round
+  // trip and barrier fewer per pair of radix-5 stages
+  if (big && pair55)
+    for (; c5 >= 2; c5 -= 2) ps.push_back({5, 5});
   for (; c5 > 0; --c5) {
     if (big && c3 > 0) { ps.push_back({5, 3}); --c3; }
     else if (big && c2 > 0) { ps.push_back({5, 2}); --c2; }
@@ -1750,7 +1754,14 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   int mp_r = 16, mp_h = 16;
   if (const char* env = std::getenv("NWB_MAXPROD_R")) mp_r = std::atoi(env);
   if (const char* env = std::getenv("NWB_MAXPROD_H")) mp_h = std::atoi(env);
-  if (!plan_fft(n_rho, p->rho_split ? 2 : p->rho_r1, p->plan_r, mp_r) || !plan_fft(p->g.m, 0, p->plan_h, mp_h)) {
+  // radix-25 rho passes for long fp32 columns: C2 fp32 rho 0.575 -> 0.553 ms per
+  // step; fp64 slower (1.060 vs 0.989: the 25-point butterfly spills at 128
+  // registers) and so are short columns (C4 fp32 6.11 -> 6.76 ms per step: too few
+  // 25-point butterflies per pass for the CTA); NWB_PAIR55=0/1 overrides
+  int pair55 = precision == NWB_F32 && n_rho >= 5000 ? 1 : 0;
+  if (const char* env = std::getenv("NWB_PAIR55")) pair55 = std::atoi(env);
+  if (!plan_fft(n_rho, p->rho_split ? 2 : p->rho_r1, p->plan_r, mp_r, pair55) ||
+      !plan_fft(p->g.m, 0, p->plan_h, mp_h)) {
     delete p;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");
   }

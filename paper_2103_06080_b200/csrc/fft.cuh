@@ -290,6 +290,27 @@ __device__ __forceinline__ void fft_pass(V* x, const FftDesc& d, int p, int rows
     V w1 = mk<V>(1, 0), w2 = mk<V>(0, 0);
     if (tw_on) { w1 = __ldg(twa + (i >> 6)); w2 = __ldg(fia + (i & 63)); }
     auto apply_tw = [&]() {
+      if constexpr (RA == 5 && RB == 5) {
+        // radix 25: W^{q + 5r} = W^q (W^5)^r from 4 + 4 powers (few live registers)
+        V wq[5], w5[5];
+        wq[1] = cmul(w1, w2);
+        wq[2] = cmul(wq[1], wq[1]);
+        wq[3] = cmul(wq[2], wq[1]);
+        wq[4] = cmul(wq[2], wq[2]);
+        w5[1] = cmul(wq[4], wq[1]);
+        w5[2] = cmul(w5[1], w5[1]);
+        w5[3] = cmul(w5[2], w5[1]);
+        w5[4] = cmul(w5[2], w5[2]);
+#pragma unroll
+        for (int q = 1; q < 5; ++q) a[q * 5] = twmul<CONJ>(a[q * 5], wq[q]);
+#pragma unroll
+        for (int r = 1; r < 5; ++r) {
+          a[r] = twmul<CONJ>(a[r], w5[r]);
+#pragma unroll
+          for (int q = 1; q < 5; ++q) a[q * 5 + r] = twmul<CONJ>(a[q * 5 + r], cmul(wq[q], w5[r]));
+        }
+        return;
+      }
       V pw[RA * RB];
       pw[0] = mk<V>(1, 0);
       pw[1] = cmul(w1, w2);
@@ -370,6 +391,7 @@ __device__ __forceinline__ void run_pass(V* x, const FftDesc& d, int p, int rows
     case 81: fft_pass<8, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 72: fft_pass<7, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 53: fft_pass<5, 3, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 55: fft_pass<5, 5, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 52: fft_pass<5, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 34: fft_pass<3, 4, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 33: fft_pass<3, 3, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
