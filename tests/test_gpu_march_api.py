@@ -40,11 +40,12 @@ def test_streamed_snapshots_equal_device_copies(cuda):
 
 
 def test_many_snapshots_do_not_grow_device_memory(cuda):
-    """101 snapshots of a Set-3 grid (72 MB each): device memory stays within
-    two snapshot buffers of a snapshot-free run; every snapshot is returned."""
+    """101 snapshots of the C2 grid (Set 4, 287 MB each, 29 GB on the host):
+    device memory stays within two snapshot buffers of a snapshot-free run;
+    every snapshot is returned."""
     import torch
 
-    c, v0 = _set(3)
+    c, v0 = _set(4)
     K = 100
     f = nw.zero_fields(K + 2, c.N_rho + 1)
     nw.run_exprk22(c, v0, f, max_steps=2)  # warm the pool
