@@ -218,11 +218,16 @@ class GpuSlabOps:
             self.red = z(2, dt=torch.int64)
 
     def close(self):
-        if getattr(self, "_h", None) and self._h.value:
-            self.lib.nwb_slab_destroy(self._h)
-            self._h = ctypes.c_void_p()
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self.lib.nwb_slab_destroy(h)
+            h.value = None
 
-    __del__ = close
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: modules may already be gone
+            pass
 
     def _run(self, fn, *args):
         import torch
