@@ -9,7 +9,7 @@ bitwise to reference goldens (tests/test_oracle.py).
 * C2 (Set 4, 10000 x 3584): K = 20 steps, fp64 on the rho-modulated N-wave
   (the bench's input) and on seed-0 turbulence, fp32 on the bench's input.
 * C4: the full 256-member ensemble on the Set-1 grid (the bench's batch size),
-  K = 10, every member's max|V| and a sample of full member fields.
+  K = 10, every member's max|V|, full field and ground metrics (peak, rise).
 * C5 (8192 x 16384) in fp32 through the rho-slab kernels, K = 3.
 """
 
@@ -102,6 +102,12 @@ def test_c4_full_ensemble_256_members(cuda, oracle):
     # every member's full field
     errs = [max_relative(ref.final[i], res.final[i]) for i in range(256)]
     assert max(errs) <= FP64_FIELD, max(errs)
+    # the ground metrics of every member (device kernel) vs the host definition
+    # on the oracle's field: N-wave peak and interpolated 10-90 % rise at rho = 144
+    for i in range(256):
+        g = nw.ground_metrics(c1, nw.Field2D(ref.final[i]))
+        assert abs(res.peak[i] - g.peak) <= 1e-10 * abs(g.peak)
+        assert abs(res.rise_theta[i] - g.rise_theta) <= 1e-8 * abs(g.rise_theta)
 
 
 def test_c5_fp32_slab_k3(cuda, oracle):
