@@ -149,6 +149,14 @@ class DevicePlan:
         ld = ref.shape[1] if ref is not None else self.n_rho
         if ref is not None and ref.shape[0] < rows:
             raise ValueError("coefficient tables have fewer rows than requested")
+        if ref is not None and not isinstance(ref, torch.Tensor) and \
+                sum(a[:rows].nbytes for a in arrays if a is not None) >= 2 * _STAGE_BYTES:
+            # large host tables (C2: 3 x 192 MB) through the page-locked staging
+            # chunks of to_device instead of a pageable copy
+            with self.on_stream():
+                arrays = [None if a is None else self.to_device(a[:rows], torch.float64)
+                          for a in arrays]
+            ref = next(a for a in arrays if a is not None)
         on_dev = int(ref is not None and isinstance(ref, torch.Tensor))
 
         def p(a):
