@@ -281,6 +281,7 @@ struct nwb_plan {
   int theta_rows_c2r = 1;    // c2r (transposed reads) favours many small CTAs for long rows
   int theta_stream_rows = 0;  // R of the streaming theta kernels (0 = not used)
   int rho_split = 0;         // 2-CTA cluster per rho column (large fp64 columns)
+  int rho_half = 0;          // k_rho_half: half-resident columns, two per SM (NWB_RHO_HALF)
   int rho_prefetch = 0;      // bulk L2 prefetch of combine operands, percent of each row (NWB_RHO_PREFETCH)
   int rho_next_pf = 0;       // L2 prefetch of column k + rho_next_pf's input (NWB_RHO_NEXTPF)
   int rho_roll = 0;          // combine: L2 prefetch of the operands rho_roll rounds ahead (NWB_RHO_ROLL)
@@ -412,6 +413,7 @@ template <typename T> RhoArgs<T> rho_args(const nwb_plan* p) {
   a.ds = (T)p->d_sigma;
   a.zero_stride = 4;
   a.split = p->rho_split;
+  a.half = p->rho_half;
   a.prefetch = p->rho_prefetch;
   a.next_pf = p->rho_next_pf;
   a.debug = p->rho_debug;
@@ -651,14 +653,14 @@ template <typename T> int create_impl(nwb_plan* p) {
   CU(cudaMemcpy(p->pos_r, pr.data(), pr.size() * sizeof(int), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(p->rev_r, fr.data(), fr.size() * sizeof(int), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(p->pos_h, ph.data(), ph.size() * sizeof(int), cudaMemcpyHostToDevice));
-  if (p->rho_split) {
+  if (p->rho_split || p->rho_half) {
     // half transform = the full plan without its leading radix-2 stage
     FftPlanHost half;
     half.stages.assign(p->plan_r.stages.begin() + 1, p->plan_r.stages.end());
     half.passes.assign(p->plan_r.passes.begin() + 1, p->plan_r.passes.end());
     std::vector<cplx<T>> tw2;
     build_desc<T>(g.nr / 2, half, p->dh2, tw2);
-    p->dh2.sym_r1 = 0;  // the split kernel reads its own half of each table row
+    if (p->rho_split) p->dh2.sym_r1 = 0;  // the split kernel reads its own half of each table row
     auto tws = twiddles<T>(g.nr, g.nr / 2);
     TRY(dalloc(p, &p->tw_h2, tw2.size() * C));
     TRY(dalloc(p, &p->tw_split, tws.size() * C));
@@ -1706,6 +1708,9 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     p->rho_split = 0;
     if (const char* env = std::getenv("NWB_RHO_SPLIT"))
       p->rho_split = (env[0] == '1' && n_rho % 2 == 0 && n_rho >= 16) ? 1 : 0;
+    if (const char* env = std::getenv("NWB_RHO_HALF"))
+      p->rho_half = (env[0] == '1' && precision == NWB_F64 && n_rho % 2 == 0 && n_rho >= 1024 &&
+                     n_rho <= 2 * 256 * 20 && !p->rho_split) ? 1 : 0;
     // bulk L2 prefetch of the combine operands: off (measured slower at Set 4
     // in both precisions since the radix-R passes and two fp32 CTAs per SM)
     p->rho_prefetch = 0;
@@ -1744,7 +1749,7 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
     int r1 = 1;
     if (const char* env = std::getenv("NWB_RHO_R1")) r1 = std::atoi(env);
     if (r1 != 2 && r1 != 4) r1 = 1;
-    if (n_rho % r1 || n_rho / r1 < 8 || p->rho_split) r1 = 1;
+    if (n_rho % r1 || n_rho / r1 < 8 || p->rho_split || p->rho_half) r1 = 1;
     // the theta CTAs hold r1 whole rows
     if ((size_t)r1 * (n_theta / 2 + 64) * 2 * (precision == NWB_F64 ? 8 : 4) > 200 * 1024) r1 = 1;
     p->rho_r1 = r1;
@@ -1760,7 +1765,8 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   // 25-point butterflies per pass for the CTA); NWB_PAIR55=0/1 overrides
   int pair55 = precision == NWB_F32 && n_rho >= 5000 ? 1 : 0;
   if (const char* env = std::getenv("NWB_PAIR55")) pair55 = std::atoi(env);
-  if (!plan_fft(n_rho, p->rho_split ? 2 : p->rho_r1, p->plan_r, mp_r, pair55) ||
+  if (precision != NWB_F32) pair55 = 0;  // radix-25 passes are compiled for fp32 only
+  if (!plan_fft(n_rho, (p->rho_split || p->rho_half) ? 2 : p->rho_r1, p->plan_r, mp_r, pair55) ||
       !plan_fft(p->g.m, 0, p->plan_h, mp_h)) {
     delete p;
     return fail(NWB_EUNSUPPORTED, "n_rho and n_theta/2 must factor into 2, 3, 5, 7");

@@ -69,15 +69,23 @@ __host__ __device__ inline int padded_len(int n, int pad_period) {
 // through xi_f^2 (the phi multipliers, bitwise symmetric) are read at the
 // canonical position, so 55-60 % of each table row is ever touched and the
 // mirrored half comes from L2 (same column, read earlier in the walk).
-__device__ __forceinline__ int sym_pos(const FftDesc& d, int p) {
-  if (d.sym_r1 <= 1) return p;
-  const int q1 = d.sym_magic ? (int)__umulhi((unsigned)p, d.sym_magic) : p;
+// the symmetry fields of a descriptor, by value (no reference to a kernel
+// parameter: taking one forces a local copy of the whole argument struct)
+struct SymInfo {
+  int r1, m;
+  unsigned magic;
+};
+__device__ __forceinline__ SymInfo sym_info(const FftDesc& d) { return SymInfo{d.sym_r1, d.sym_m, d.sym_magic}; }
+__device__ __forceinline__ int sym_pos(SymInfo d, int p) {
+  if (d.r1 <= 1) return p;
+  const int q1 = d.magic ? (int)__umulhi((unsigned)p, d.magic) : p;
   if (q1 == 0) return p;
-  const int rest = p - q1 * d.sym_m;
-  const int q2 = d.sym_r1 - q1;
-  if (q1 < q2 || (q1 == q2 && 2 * rest <= d.sym_m - 1)) return p;
-  return q2 * d.sym_m + (d.sym_m - 1 - rest);
+  const int rest = p - q1 * d.m;
+  const int q2 = d.r1 - q1;
+  if (q1 < q2 || (q1 == q2 && 2 * rest <= d.m - 1)) return p;
+  return q2 * d.m + (d.m - 1 - rest);
 }
+__device__ __forceinline__ int sym_pos(const FftDesc& d, int p) { return sym_pos(sym_info(d), p); }
 
 // ------------------------------------------------------------ butterflies
 // Forward uses w = exp(-2 pi i / r); INV uses the conjugate.
@@ -391,7 +399,9 @@ __device__ __forceinline__ void run_pass(V* x, const FftDesc& d, int p, int rows
     case 81: fft_pass<8, 1, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 72: fft_pass<7, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 53: fft_pass<5, 3, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
-    case 55: fft_pass<5, 5, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
+    case 55:  // fp32 only (the host planner never emits it for fp64: register budget)
+      if constexpr (sizeof(V) == 8) fft_pass<5, 5, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth);
+      break;
     case 52: fft_pass<5, 2, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 34: fft_pass<3, 4, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;
     case 33: fft_pass<3, 3, DIT, CONJ>(x, d, p, rows, rstride, tw, tid, nth); break;

@@ -86,6 +86,7 @@ template <typename T> struct RhoArgs {
   const cplx<T>* tw_h2;
   const cplx<T>* tw_split;
   int split;
+  int half;                   // k_rho_half: half the column in registers, two columns per SM
   int prefetch;               // bulk L2 prefetch of the combine operands at entry: percent of each row
   int next_pf;                // > 0: prefetch the input column k + next_pf into L2 after the combine
   int roll;                   // > 0: the combine prefetches its operands roll rounds ahead into L2

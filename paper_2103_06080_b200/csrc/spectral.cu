@@ -470,7 +470,7 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
                                             cplx<T>* __restrict__ vh, cplx<T>* __restrict__ u,
                                             T ds, int debug, int tid = threadIdx.x,
                                             int nth = blockDim.x, int roll = 0,
-                                            const FftDesc* dsym = nullptr, int pofs = 0) {
+                                            SymInfo dsym = SymInfo{-1, 0, 0u}, int pofs = 0) {
   using V = cplx<T>;
   constexpr int U = 4;
   const bool nl = debug & 2;
@@ -500,7 +500,7 @@ __device__ __forceinline__ void rho_combine(cplx<T>* x, const FftDesc& d, int n,
         sp[q] = XG ? p : pidx(d, p);
         b[q] = x[sp[q]];
         // tables: canonical +-f position (sub-columns: of global position pofs + p)
-        const int tp = dsym ? sym_pos(*dsym, pofs + p) : sym_pos(d, p);
+        const int tp = dsym.r1 >= 0 ? sym_pos(dsym, pofs + p) : sym_pos(d, p);
         if (MODE == RHO_STAGE1 && !nl) {
           o1[q] = E[tp]; o2[q] = vh[p]; o3[q] = P1[tp]; o4[q] = P12[tp];
         } else if (MODE == RHO_STAGE2) {
@@ -669,6 +669,236 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
 }
 
+// ------------------------------------------------------------------ rho pass, half-resident columns
+// Two fp64 columns per SM with the whole column on chip: a 256-thread CTA
+// keeps one half of its column in an 80 KB shared-memory line and parks the
+// other half in TENSOR MEMORY (tcgen05.st / tcgen05.ld, 160 of the CTA's 256
+// allocated TMEM columns; TMEM is 256 KB per SM and otherwise unused here), so
+// two CTAs -- two columns, one streaming while the other transforms -- share
+// an SM where k_rho fits one 160 KB column.  Thread t owns the indices
+// s = t + 256 q (q < KPT); with the plan's first stage radix 2 (positions
+// q1 n/2 + p'):
+//   load   y0 = x_s + x_{s+M} -> TMEM, y1 = (x_s - x_{s+M}) W_n^s -> line
+//   FFT y1 (line); swap TMEM <-> line (own index set); FFT y0 (line)
+//   combine  y0 half in the line (positions p'), y1 half in TMEM (M + s)
+//   inverse y0 (DIT, natural out); swap; inverse y1
+//   store  x_s = z0 + conj(W_n^s) z1, x_{s+M} = z0 - conj(W_n^s) z1
+// TMEM moves 4 complex (16 32-bit words) per tcgen05.{st,ld}.32x32b.x16; a
+// warp reaches its lane quarter (warp mod 4), warps w and w + 4 use disjoint
+// column ranges.
+constexpr int HALF_NT = 256;
+constexpr int HALF_CHUNK = 4;  // complex per TMEM transfer
+
+__device__ __forceinline__ void tmem_st16(unsigned taddr, const double2 (&v)[HALF_CHUNK]) {
+  unsigned w[16];
+#pragma unroll
+  for (int i = 0; i < HALF_CHUNK; ++i) {
+    w[4 * i + 0] = (unsigned)__double2loint(v[i].x);
+    w[4 * i + 1] = (unsigned)__double2hiint(v[i].x);
+    w[4 * i + 2] = (unsigned)__double2loint(v[i].y);
+    w[4 * i + 3] = (unsigned)__double2hiint(v[i].y);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};\n" ::"r"(taddr),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+      "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, double2 (&v)[HALF_CHUNK]) {
+  unsigned w[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];\n"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]),
+        "=r"(w[14]), "=r"(w[15])
+      : "r"(taddr)
+      : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < HALF_CHUNK; ++i) {
+    v[i].x = __hiloint2double((int)w[4 * i + 1], (int)w[4 * i + 0]);
+    v[i].y = __hiloint2double((int)w[4 * i + 3], (int)w[4 * i + 2]);
+  }
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+}
+
+template <int MODE, int KPT>
+__global__ void __launch_bounds__(HALF_NT, 2) k_rho_half(const RhoArgs<double> a) {
+  using V = double2;
+  static_assert(KPT % HALF_CHUNK == 0, "KPT must be a multiple of the TMEM chunk");
+  constexpr int NCH = KPT / HALF_CHUNK;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ unsigned tmem_base_sh;
+  V* x = reinterpret_cast<V*>(smem_raw);
+  const FftDesc& d = a.dh2;
+  const int M = d.n, t = threadIdx.x, warp = t >> 5;
+  const int mem = blockIdx.x, k = blockIdx.y;
+  const size_t row = ((size_t)mem * a.g.kk + k) * a.g.ld;
+  const size_t trow = (size_t)k * a.g.ld;
+  if (a.stagger_ns > 0) {
+    const int slot = blockIdx.x + blockIdx.y * gridDim.x;
+    if (slot < a.stagger_slots) {
+      const long long wait = (long long)slot * a.stagger_ns / a.stagger_slots;
+      if (t == 0 && wait > 0) {
+        unsigned long long t0, tn;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+          __nanosleep(500);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+        } while ((long long)(tn - t0) < wait);
+      }
+      __syncthreads();
+    }
+  }
+  // TMEM: 256 columns for this CTA (two CTAs per SM fill the 512)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;\n" ::"r"(
+                     smem_u32(&tmem_base_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  // this warp's lane quarter and column range: 4 words per complex
+  const unsigned tbase = tmem_base_sh + ((unsigned)(32 * (warp & 3)) << 16) +
+                         (unsigned)((warp >> 2) * KPT * 4);
+  auto col = [&](int c) { return tbase + (unsigned)(c * HALF_CHUNK * 4); };
+  auto sidx_of = [&](int c, int i) { return t + HALF_NT * (c * HALF_CHUNK + i); };
+
+  // load + first radix-2 DIF stage
+  const V* src = a.in + row;
+#pragma unroll 1
+  for (int c = 0; c < NCH; ++c) {
+    V y0[HALF_CHUNK];
+#pragma unroll
+    for (int i = 0; i < HALF_CHUNK; ++i) {
+      const int si = sidx_of(c, i);
+      y0[i] = mk<V>(0, 0);
+      if (si < M) {
+        const V x0 = src[si], x1 = src[si + M];
+        y0[i] = cadd(x0, x1);
+        x[pidx(d, si)] = cmul(csub(x0, x1), __ldg(&a.tw_split[si]));
+      }
+    }
+    tmem_st16(col(c), y0);
+  }
+  tmem_wait_st();
+  if (a.zero_bits && k == 0 && t == 0) a.zero_bits[(size_t)mem * a.zero_stride] = 0ULL;
+  __syncthreads();
+  // swap: y1_hat (line) <-> y0 (TMEM), own index set
+  auto swap_line_tmem = [&]() {
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+      V tv[HALF_CHUNK], lv[HALF_CHUNK];
+      tmem_ld16(col(c), tv);
+#pragma unroll
+      for (int i = 0; i < HALF_CHUNK; ++i) {
+        const int si = sidx_of(c, i);
+        lv[i] = mk<V>(0, 0);
+        if (si < M) {
+          const int ps = pidx(d, si);
+          lv[i] = x[ps];
+          x[ps] = tv[i];
+        }
+      }
+      tmem_st16(col(c), lv);
+    }
+    tmem_wait_st();
+  };
+  // one call site per transform direction (a second call site would copy
+  // the kernel-parameter descriptor to local memory)
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    fft_forward(x, d, 1, 0, a.tw_h2);
+    if (h == 0) {
+      swap_line_tmem();
+      __syncthreads();
+    }
+  }
+  // combine: the y0 half in the line (positions p' < M) ...
+  const SymInfo sym = sym_info(a.dr);
+  rho_combine<double, MODE>(x, d, M, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
+                            a.vh + row, a.u + row, a.ds, 0, t, HALF_NT, 0, sym, 0);
+  // ... and the y1 half in TMEM (positions M + s)
+  {
+    const V* E = a.E + trow;
+    const V* P1 = a.P1 + trow;
+    const V* P12 = a.P12 + trow;
+    const V* P2 = a.P2 + trow;
+    V* vh = a.vh + row;
+    V* u = a.u + row;
+    const double ds = a.ds;
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+      V bv[HALF_CHUNK];
+      tmem_ld16(col(c), bv);
+#pragma unroll
+      for (int i = 0; i < HALF_CHUNK; ++i) {
+        const int si = sidx_of(c, i);
+        if (si >= M) continue;
+        const int p = M + si;
+        const int tp = sym_pos(sym, p);
+        const V bb = bv[i];
+        if (MODE == RHO_STAGE1) {
+          const V ev = cmul(E[tp], vh[p]);
+          const V p12 = P12[tp], p1 = P1[tp];
+          u[p] = cadd(ev, cmul(mk<V>(ds * p12.x, ds * p12.y), bb));
+          bv[i] = cadd(ev, cmul(mk<V>(ds * p1.x, ds * p1.y), bb));
+        } else if (MODE == RHO_STAGE2) {
+          const V p2 = P2[tp];
+          const V vn = cadd(u[p], cmul(mk<V>(ds * p2.x, ds * p2.y), bb));
+          vh[p] = vn;
+          bv[i] = vn;
+        } else if (MODE == RHO_EULER) {
+          const V p1 = P1[tp];
+          const V vn = cadd(cmul(E[tp], vh[p]), cmul(mk<V>(ds * p1.x, ds * p1.y), bb));
+          vh[p] = vn;
+          bv[i] = vn;
+        } else if (MODE == RHO_INIT) {
+          vh[p] = bb;
+        }
+      }
+      tmem_st16(col(c), bv);
+    }
+    tmem_wait_st();
+  }
+  __syncthreads();
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    fft_inverse(x, d, 1, 0, a.tw_h2);  // h = 0: z0, h = 1: z1, natural order
+    if (h == 0) {
+      swap_line_tmem();  // z0 -> TMEM, y1 combined -> line
+      __syncthreads();
+    }
+  }
+  V* dst = a.out + row;
+#pragma unroll 1
+  for (int c = 0; c < NCH; ++c) {
+    V z0[HALF_CHUNK];
+    tmem_ld16(col(c), z0);
+#pragma unroll
+    for (int i = 0; i < HALF_CHUNK; ++i) {
+      const int si = sidx_of(c, i);
+      if (si < M) {
+        const V z1 = cmulc(x[pidx(d, si)], __ldg(&a.tw_split[si]));
+        dst[si] = cadd(z0[i], z1);
+        dst[si + M] = csub(z0[i], z1);
+      }
+    }
+  }
+  if (a.step_ctr && mem == 0 && k == 0 && t == 0) *a.step_ctr += 1;
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;\n" ::"r"(tmem_base_sh)
+                 : "memory");
+}
+
 // ------------------------------------------------------------------ rho pass, sub-columns
 // With the first rho stage fused into the theta passes (ThetaArgs::r1), a rho
 // column k splits into r1 independent msub-point sub-columns: position
@@ -721,8 +951,8 @@ __global__ void __launch_bounds__(256, rho_sub_min_blocks<T>()) k_rho_sub(const 
   }
   if (MODE != RHO_INV_NAT)
     rho_combine<T, MODE>(x, d, ms, a.E + trow, a.P1 + trow, a.P12 + trow, a.P2 + trow,
-                         a.vh + sub, a.u + sub, a.ds, 0, threadIdx.x, blockDim.x, 0, &a.dr,
-                         q1 * ms);
+                         a.vh + sub, a.u + sub, a.ds, 0, threadIdx.x, blockDim.x, 0,
+                         sym_info(a.dr), q1 * ms);
   __syncthreads();
   fft_inverse(x, d, 1, 0, a.tw_sub);
   const int js = a.ilv ? r1 : 1;
@@ -1114,6 +1344,15 @@ template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cud
 
 template <typename T, int MODE>
 static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
+  if constexpr (MODE <= RHO_INIT && sizeof(T) == 8) {
+    if (a.half && a.dh2.n <= HALF_NT * 20) {
+      const size_t sm = (size_t)padded_len(a.dh2.n, a.dh2.pad_period) * sizeof(cplx<T>);
+      cudaFuncSetAttribute(k_rho_half<MODE, 20>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      dim3 grid(a.g.batch, a.g.kk);
+      k_rho_half<MODE, 20><<<grid, HALF_NT, sm, s>>>(a);
+      return;
+    }
+  }
   if constexpr (MODE != RHO_REV2NAT && MODE != RHO_FWD_NAT) {
     if (a.r1 > 1) {
       const size_t sm = (size_t)padded_len(a.dsub.n, a.dsub.pad_period) * sizeof(cplx<T>);

@@ -14,7 +14,7 @@ sys.path.insert(0, ROOT)
 import paper_2103_06080_b200 as P  # noqa: E402
 from paper_2103_06080_b200.plan import DevicePlan  # noqa: E402
 
-KNOBS = ("NWB_PAIR55", "NWB_RHO_BULK", "NWB_THETA_BULK", "NWB_RHO_STAGGER", "NWB_RHO_DEBUG", "NWB_RHO_PREFETCH", "NWB_RHO_NEXTPF", "NWB_RHO_ROLL", "NWB_RHO_WS", "NWB_RHO_WS_DEBUG", "NWB_RHO_SYM", "NWB_RHO_THREADS", "NWB_RHO_SPLIT", "NWB_RHO_PERSIST",
+KNOBS = ("NWB_RHO_HALF", "NWB_PAIR55", "NWB_RHO_BULK", "NWB_THETA_BULK", "NWB_RHO_STAGGER", "NWB_RHO_DEBUG", "NWB_RHO_PREFETCH", "NWB_RHO_NEXTPF", "NWB_RHO_ROLL", "NWB_RHO_WS", "NWB_RHO_WS_DEBUG", "NWB_RHO_SYM", "NWB_RHO_THREADS", "NWB_RHO_SPLIT", "NWB_RHO_PERSIST",
          "NWB_MAXPROD_R", "NWB_MAXPROD_H", "NWB_THETA_ROWS", "NWB_THETA_ROWS_C2R", "NWB_THETA_THREADS", "NWB_THETA_STREAM", "NWB_THETA_DEBUG", "NWB_PAD", "NWB_PAD_N")
 
 
