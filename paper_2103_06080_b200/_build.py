@@ -74,8 +74,11 @@ def build(force: bool = False, verbose: bool = False, ptxas_v: bool = False,
     lib_path = out or LIB_PATH
     if not force and not defines and out is None and up_to_date():
         return LIB_PATH
-    build_dir = BUILD_DIR + ("_" + os.path.basename(lib_path).replace(".so", "") if out else "")
+    # variants get their own object directory, keyed by the whole output path
+    tag = os.path.abspath(lib_path).replace(".so", "").strip(os.sep).replace(os.sep, "_")
+    build_dir = BUILD_DIR + ("_" + tag if out else "")
     os.makedirs(build_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(os.path.abspath(lib_path)), exist_ok=True)
     objs = []
     procs = []
     headers = [d for d in _sources() if not d.endswith(".cu")]

@@ -519,3 +519,33 @@ def test_transforms_vs_cufft(cuda, shape):
     ref_back = torch.fft.irfft2(ref, s=shape)
     err = float((back - ref_back).abs().max() / ref_back.abs().max())
     assert err <= 1e-14, err
+
+
+@pytest.mark.parametrize("n_rho,batch", [(2000, 1), (1250, 2)])
+def test_rho_half_tmem_vs_oracle(cuda, oracle, monkeypatch, n_rho, batch):
+    """The TMEM half-column rho kernel (k_rho_half, NWB_RHO_HALF=1, off by
+    default): a turbulent ExpRK22 march against the oracle (north-star bar) and
+    against the default rho kernel (same arithmetic, other FFT grouping)."""
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    cfg = nw.DomainConfig(N_rho=n_rho, N_theta=64, N_sigma=5, Sigma=2.0)
+    sig, rho, theta = nw.build_axes(cfg)
+    spec = nw.sample_modes(nw.TurbulenceParams(seed=3))
+    f = nw.evaluate_fields(spec, spec.lam, sig, nw.rho_nodes_closed(cfg))
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B), depth=0.3).values
+    v0s = np.stack([v0 * (1.0 + 0.05 * i) for i in range(batch)])
+    outs = []
+    for half in ("0", "1"):
+        monkeypatch.setenv("NWB_RHO_HALF", half)
+        plan = DevicePlan(n_rho, cfg.N_theta, batch, "double", cfg.d_sigma, cfg.rho_span,
+                          cfg.theta_span, cfg.A, cfg.B, nw.EPS_DOUBLE)
+        plan.set_coeffs(f.u_par, f.u_perp, f.du_perp_drho)
+        plan.load_physical(v0s if batch > 1 else v0)
+        plan.march("exprk22", 0, cfg.N_sigma)
+        out, _ = plan.store_physical()
+        outs.append(out.cpu().numpy().reshape(batch, n_rho, cfg.N_theta))
+        plan.close()
+    for i in range(batch):
+        assert max_relative(outs[0][i], outs[1][i]) <= FP64_KERNEL
+        ref = oracle.march(cfg, v0s[i], f)
+        assert max_relative(ref.final, outs[1][i]) <= FP64_FIELD
