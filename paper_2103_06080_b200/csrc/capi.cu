@@ -1804,7 +1804,8 @@ int nwb_plan_create(nwb_plan** out, int n_rho, int n_theta, int batch, int preci
   // per SM, rho pass 2.97 -> 1.45 ms per 256-member stage) while the 10000-point
   // C2 column keeps 512 threads (measured best against 256 / 384 / 640 / 768)
   int th = ((n_rho / 10) + 31) / 32 * 32;
-  p->rho_threads = th < 128 ? 128 : (th > 512 ? 512 : th);  // small grids: latency-bound, keep 4 warps
+  const int th_max = precision == NWB_F32 ? 384 : 512;  // fp32: k_rho_r80 (spectral.cu)
+  p->rho_threads = th < 128 ? 128 : (th > th_max ? th_max : th);  // small grids: latency-bound, keep 4 warps
   if (p->rho_split) p->rho_threads = p->rho_threads > 256 ? 256 : p->rho_threads;
   if (p->rho_r1 > 1) {  // sub-columns: about one radix-10 butterfly per thread, <= 256
     const int ts = ((p->msub / 10) + 31) / 32 * 32;

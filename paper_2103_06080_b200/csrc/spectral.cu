@@ -49,9 +49,6 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 #define NWB_THETA_MINB64 2
 #endif
 
-#ifndef NWB_RHO_THREADS_LB
-#define NWB_RHO_THREADS_LB 512
-#endif
 // threads per theta CTA: 128 per staged row up to 256 (one-row CTAs are
 // small, so more of them -- in different phases -- share an SM)
 template <int R> constexpr int theta_threads() { return R == 1 ? 128 : 256; }
@@ -576,7 +573,7 @@ __device__ __forceinline__ void column_bulk_store(V* dst, const FftDesc& d, cons
 }
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho(const RhoArgs<T> a) {
+__device__ __forceinline__ void rho_column(const RhoArgs<T>& a) {
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long load_bar;
@@ -667,6 +664,19 @@ __global__ void __launch_bounds__(NWB_RHO_THREADS_LB, rho_min_blocks<T>()) k_rho
   else if (!(a.debug & 4))
     for (int j = threadIdx.x; j < n; j += blockDim.x) dst[j] = x[pidx(a.dr, j)];
   if (a.step_ctr && mem == 0 && k == 0 && threadIdx.x == 0) *a.step_ctr += 1;
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(512, rho_min_blocks<T>()) k_rho(const RhoArgs<T> a) {
+  rho_column<T, MODE>(a);
+}
+// fp32 columns of >= 384 threads (two CTAs per SM): a 384-thread bound gives
+// the FFT 80 registers instead of 64 (232-byte spills): C2 fp32 rho 0.560 ->
+// 0.543 ms per step.  Short fp32 columns keep k_rho (64 registers, more CTAs
+// per SM: C4 fp32 6.33 -> 6.13 ms per step).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(384, 2) k_rho_r80(const RhoArgs<T> a) {
+  rho_column<T, MODE>(a);
 }
 
 // ------------------------------------------------------------------ rho pass, half-resident columns
@@ -1397,8 +1407,15 @@ static void rho_m(const RhoArgs<T>& a, int threads, cudaStream_t s) {
     }
   }
   const size_t sm = (size_t)padded_len(a.dr.n, a.dr.pad_period) * sizeof(cplx<T>);
-  cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   dim3 grid(a.g.batch, a.k_cnt > 0 ? a.k_cnt : a.g.kk - a.k_off);
+  if constexpr (sizeof(T) == 4) {
+    if (threads >= 384) {
+      cudaFuncSetAttribute(k_rho_r80<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_rho_r80<T, MODE><<<grid, 384, sm, s>>>(a);
+      return;
+    }
+  }
+  cudaFuncSetAttribute(k_rho<T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_rho<T, MODE><<<grid, threads, sm, s>>>(a);
   }
 }

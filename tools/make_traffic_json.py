@@ -14,7 +14,7 @@ import subprocess
 import sys
 
 GROUPS = {"k_theta_c2r": "theta_c2r", "k_theta_r2c": "theta_r2c", "k_weno": "weno", "k_weno_x2": "weno",
-          "k_rho": "rho_pass"}
+          "k_rho": "rho_pass", "k_rho_r80": "rho_pass"}
 
 
 def scale(v, unit):
