@@ -52,6 +52,11 @@ __device__ __forceinline__ void block_max2(u64 a, u64 b, u64* dst_a, u64* dst_b)
 // threads per theta CTA: 128 per staged row up to 256 (one-row CTAs are
 // small, so more of them -- in different phases -- share an SM)
 template <int R> constexpr int theta_threads() { return R == 1 ? 128 : 256; }
+// elements per batch of independent table loads in the theta pre / post loops
+#ifndef NWB_POST_UB
+#define NWB_POST_UB 4
+#endif
+constexpr int POST_UB = NWB_POST_UB;
 // five one-row fp64 CTAs per SM (96 registers, a 60-byte spill in the FFT
 // driver): C2 theta-c2r 0.233 -> 0.226 ms against four (C1 / C4 unchanged)
 #ifndef NWB_THETA_MINB_R1
@@ -94,15 +99,26 @@ __device__ __forceinline__ void c2r_pre(cplx<T>* z, const ThetaArgs<T>& a, int r
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     V* zr = z + r * rs;
-    for (int k = threadIdx.x; k < npairs; k += blockDim.x) {
-      const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
-      V xk = zr[sk];
-      V xm = zr[sm];
-      if (k == 0) { xk.y = 0; xm.y = 0; }
-      const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
-      const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), __ldg(&a.wk[k]));
-      zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
-      if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
+    for (int k0 = threadIdx.x; k0 < npairs; k0 += POST_UB * blockDim.x) {
+      V w[POST_UB];
+#pragma unroll
+      for (int u = 0; u < POST_UB; ++u) {
+        const int k = k0 + u * blockDim.x;
+        w[u] = __ldg(&a.wk[k < npairs ? k : 0]);
+      }
+#pragma unroll
+      for (int u = 0; u < POST_UB; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k >= npairs) break;
+        const int sk = pidx(a.dh, k), sm = pidx(a.dh, m - k);
+        V xk = zr[sk];
+        V xm = zr[sm];
+        if (k == 0) { xk.y = 0; xm.y = 0; }
+        const V ze = mk<V>(xk.x + xm.x, xk.y - xm.y);
+        const V zo = cmulc(mk<V>(xk.x - xm.x, xk.y + xm.y), w[u]);
+        zr[sk] = mk<V>(ze.x - zo.y, ze.y + zo.x);
+        if (k != 0 && 2 * k != m) zr[sm] = mk<V>(ze.x + zo.y, zo.x - ze.y);
+      }
     }
   }
 }
@@ -125,16 +141,29 @@ __device__ __forceinline__ void c2r_post(const cplx<T>* z, const ThetaArgs<T>& a
     V* drow = reinterpret_cast<V*>(dst + (size_t)j * a.g.nt);
     T hi = -INFINITY, lo = INFINITY;
     bool nan = false;
-    for (int n = threadIdx.x; n < m; n += blockDim.x) {
-      const V zz = zr[pidx(a.dh, __ldg(&a.pos_h[n]))];
-      const T v0 = zz.x * scale, v1 = zz.y * scale;
-      drow[n] = mk<V>(v0, v1);
-      // plain compares (NaNs are caught by the flag below)
-      const bool o = v0 > v1;
-      const T mx = o ? v0 : v1, mn = o ? v1 : v0;
-      hi = mx > hi ? mx : hi;
-      lo = mn < lo ? mn : lo;
-      nan |= (v0 != v0) | (v1 != v1);
+    // the digit-reversal positions of POST_UB elements are loaded up front (one
+    // batch of independent loads instead of a load -> use chain per element)
+    for (int n0 = threadIdx.x; n0 < m; n0 += POST_UB * blockDim.x) {
+      int ps[POST_UB];
+#pragma unroll
+      for (int u = 0; u < POST_UB; ++u) {
+        const int n = n0 + u * blockDim.x;
+        ps[u] = n < m ? __ldg(&a.pos_h[n]) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < POST_UB; ++u) {
+        const int n = n0 + u * blockDim.x;
+        if (n >= m) break;
+        const V zz = zr[pidx(a.dh, ps[u])];
+        const T v0 = zz.x * scale, v1 = zz.y * scale;
+        drow[n] = mk<V>(v0, v1);
+        // plain compares (NaNs are caught by the flag below)
+        const bool o = v0 > v1;
+        const T mx = o ? v0 : v1, mn = o ? v1 : v0;
+        hi = mx > hi ? mx : hi;
+        lo = mn < lo ? mn : lo;
+        nan |= (v0 != v0) | (v1 != v1);
+      }
     }
     if (threadIdx.x < m) {
       const T c = up ? two_pi * up[j] : (T)0;
@@ -223,19 +252,34 @@ __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a
   V* dst = a.spec_out + (size_t)mem * a.g.kk * ld;
   const int npairs = m / 2 + 1;
   const T half = (T)0.5;
-  for (int idx = threadIdx.x; idx < npairs * R; idx += blockDim.x) {
-    const int r = idx % R, k = idx / R, j = j0 + r;
-    if (j >= jend) continue;
-    const V* zr = z + r * rs;
-    const V zk = zr[pidx(a.dh, __ldg(&a.pos_h[k]))];
-    const V zm = zr[pidx(a.dh, __ldg(&a.pos_h[k == 0 ? 0 : m - k]))];
-    const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
-    const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
-    const V wz = cmul(__ldg(&a.wk[k]), zo);
-    dst[(size_t)k * ld + j] = cadd(ze, wz);
-    if (2 * k != m) {
-      const V d = csub(ze, wz);
-      dst[(size_t)(m - k) * ld + j] = mk<V>(d.x, -d.y);
+  // positions and twiddles of POST_UB pairs are loaded up front (independent loads)
+  for (int i0 = threadIdx.x; i0 < npairs * R; i0 += POST_UB * blockDim.x) {
+    int pk[POST_UB], pm[POST_UB];
+    V wk[POST_UB];
+#pragma unroll
+    for (int u = 0; u < POST_UB; ++u) {
+      const int idx = i0 + u * blockDim.x, k = idx < npairs * R ? idx / R : 0;
+      pk[u] = __ldg(&a.pos_h[k]);
+      pm[u] = __ldg(&a.pos_h[k == 0 ? 0 : m - k]);
+      wk[u] = __ldg(&a.wk[k]);
+    }
+#pragma unroll
+    for (int u = 0; u < POST_UB; ++u) {
+      const int idx = i0 + u * blockDim.x;
+      if (idx >= npairs * R) break;
+      const int r = idx % R, k = idx / R, j = j0 + r;
+      if (j >= jend) continue;
+      const V* zr = z + r * rs;
+      const V zk = zr[pidx(a.dh, pk[u])];
+      const V zm = zr[pidx(a.dh, pm[u])];
+      const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
+      const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
+      const V wz = cmul(wk[u], zo);
+      dst[(size_t)k * ld + j] = cadd(ze, wz);
+      if (2 * k != m) {
+        const V d = csub(ze, wz);
+        dst[(size_t)(m - k) * ld + j] = mk<V>(d.x, -d.y);
+      }
     }
   }
 }
