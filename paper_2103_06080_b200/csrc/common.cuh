@@ -151,6 +151,15 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 // complex loads/stores of 16-byte (double2) or 8-byte (float2) elements
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem_src) : "memory");
+}
+// one real (8 or 4 bytes)
+template <typename T> __device__ __forceinline__ void cp_async_real(T* dst, const T* src) {
+  if constexpr (sizeof(T) == 8) cp_async8(dst, src);
+  else cp_async4(dst, src);
+}
 template <typename V> __device__ __forceinline__ void cp_async_c(V* dst, const V* src) {
   if constexpr (sizeof(V) == 16) cp_async16(dst, src);
   else cp_async8(dst, src);

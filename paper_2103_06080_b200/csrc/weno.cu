@@ -129,6 +129,9 @@ constexpr int WWARPS = 4;   // warps per CTA, stacked along rho
 #ifndef NWB_WENO_MINB
 #define NWB_WENO_MINB 1
 #endif
+#ifndef NWB_WENO_CPASYNC
+#define NWB_WENO_CPASYNC 1
+#endif
 // WTR: rows per warp tile (32; 16 / 8 for small grids, where more, shorter warps
 // finish sooner -- the extra rho halo and faces are cheap there)
 //
@@ -182,12 +185,23 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
 
   if constexpr (WALK) {
     // ---- theta faces, lane r walks row r: stage the tile's V (slot s = column x0 + s - 3)
+#if NWB_WENO_CPASYNC
+    // as asynchronous copies: all of the lane's 32-38 loads in flight at once,
+    // no register round trip (the staging stalled on each batch of loads)
+    for (int r = 0; r < rows; ++r) {
+      const T* vr = v + (size_t)vrow(j0 + r) * nt;
+      cp_async_real(&ftw[r][lane], vr + kl);
+      if (lane < 6) cp_async_real(&ftw[r][32 + lane], vr + kh);
+    }
+    cp_async_wait_all();
+#else
 #pragma unroll 8
     for (int r = 0; r < rows; ++r) {
       const T* vr = v + (size_t)vrow(j0 + r) * nt;
       ftw[r][lane] = vr[kl];
       if (lane < 6) ftw[r][32 + lane] = vr[kh];
     }
+#endif
     __syncwarp();
     if (lane < rows) {
       const T c = mul_rn(pi, upar[j0 + lane]);
@@ -439,6 +453,15 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
   const int rows = min(WTR, jend - j0);
 
   if constexpr (WALK) {
+#if NWB_WENO_CPASYNC
+    for (int r = 0; r < rows; ++r) {
+      const T* vr = v + (size_t)vrow(j0 + r) * nt;
+      cp_async_real(&ftw[r][lane], vr + kl0);
+      cp_async_real(&ftw[r][lane + 32], vr + kl1);
+      if (lane < 6) cp_async_real(&ftw[r][64 + lane], vr + kh);
+    }
+    cp_async_wait_all();
+#else
 #pragma unroll 8
     for (int r = 0; r < rows; ++r) {
       const T* vr = v + (size_t)vrow(j0 + r) * nt;
@@ -446,6 +469,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
       ftw[r][lane + 32] = vr[kl1];
       if (lane < 6) ftw[r][64 + lane] = vr[kh];
     }
+#endif
     __syncwarp();
     if (lane < rows) {
       const T c = mul_rn(pi, upar[j0 + lane]);

@@ -1,5 +1,5 @@
-# developer A/B: batched table loads in the theta pre/post loops
-for L in variants/base/libnwb200.so "" variants/ub8/libnwb200.so; do
+# developer A/B: WENO tile staging by cp.async
+for L in variants/base/libnwb200.so ""; do
   echo "== lib ${L:-default}"
   for p in double single; do
     NWB_LIB=$L python tools/rho_probe.py $p "" 2>&1 | grep -v Warn
@@ -8,3 +8,4 @@ for L in variants/base/libnwb200.so "" variants/ub8/libnwb200.so; do
 done
 python -m pytest -q -x tests/test_gpu_parity.py 2>&1 | tail -n 1
 python -m pytest -q -x tests/test_gpu_bench_configs.py -k c2 2>&1 | tail -n 1
+python -m pytest -q -x tests/test_gpu_slab.py tests/test_gpu_reference_ports.py 2>&1 | tail -n 1

@@ -3,7 +3,7 @@
 # aggregated by SASS opcode on the box.  Usage: bash tools/opmix_r02.sh TAG
 T=${1:-r02}
 mkdir -p gpurun_out
-for K in "k_rho" "k_theta_c2r" "k_theta_r2c"; do
+for K in ${KERNELS:-k_rho k_theta_c2r k_theta_r2c}; do
   ncu --section SourceCounters --section WarpStateStats --clock-control none --import-source on \
       --kernel-name-base demangled -k regex:"${K}<" --launch-skip 4 -c 1 -f -o gpurun_out/${T}_src_${K} \
       python tools/rho_probe.py double "" > gpurun_out/${T}_src_${K}.log 2>&1
