@@ -98,8 +98,10 @@ int nwb_plan_store_physical(nwb_plan* plan, void* v_dev, double* max_abs_host);
  *     device buffers (batch, n_rho, n_theta).
  *   max_abs_host: [batch * n_steps] max|V_n| per member and step (or NULL).
  *   step_ms_host: [n_steps * 3] = (step, nonlinear, linear) device ms from
- *     CUDA events recorded by the replayed step graph, or NULL (graph replay
- *     without events).
+ *     %globaltimer stamps the march kernels write at entry (step start, WENO
+ *     start, theta r2c start = WENO end, per stage; nonlinear = the WENO
+ *     time like exprk.py:176), read back once after the march; or NULL.  The
+ *     same step graph is replayed either way.
  *   guard: stop with NWB_EINSTABILITY at the first step whose max|V_n| is
  *     non-finite or > guard; *fail_step, *fail_member, *fail_value say where
  *     (the message carries "step=<n> member=<i> max_abs=<v>").

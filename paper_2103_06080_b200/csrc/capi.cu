@@ -318,20 +318,10 @@ struct nwb_plan {
   // graphs (one captured step per scheme)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   cudaStream_t graph_stream[2] = {nullptr, nullptr};
-  // timed graphs: the same step with external event-record nodes at the stage
-  // bucket boundaries; each replay points the nodes at that step's events
-  // (cudaGraphExecEventRecordNodeSetEvent), so the drop-in default path
-  // (per-step nonlinear / linear buckets) still runs from a CUDA graph
-  // NTG instances per scheme are replayed round robin: an instance's event nodes
-  // are re-pointed only after its previous replay has finished (re-pointing a
-  // node whose replay is still in flight fails with cudaErrorInvalidValue)
-  static constexpr int NTG = 4;
-  cudaGraph_t tgraph_g[2] = {nullptr, nullptr};
-  cudaGraphExec_t tgraph[2][NTG] = {};
-  cudaStream_t tgraph_stream[2] = {nullptr, nullptr};
-  cudaGraphNode_t tnode[2][10] = {};
-  cudaEvent_t tev[10] = {};          // placeholder events recorded during capture
-  bool ev_external = false;          // capturing: record events as external nodes
+  // per-step bucket time stamps [hist_len + 1][NWB_TS_SLOTS] (internal.h
+  // StepStamp): written by the march kernels themselves, so the timed default
+  // path replays the same graph as the untimed one
+  unsigned long long* stamps = nullptr;
   std::vector<void*> allocs;
 };
 
@@ -464,25 +454,19 @@ template <typename T> WenoArgs<T> weno_args(const nwb_plan* p) {
 // ev (optional) holds 5 events: before c2r and after each of the 4 kernels.
 constexpr int EV_PER_STAGE = 5;
 
-inline void rec_event(const nwb_plan* p, cudaEvent_t e, cudaStream_t s) {
-  if (!e) return;  // the timed graph records only the bucket boundaries it needs
-  if (p->ev_external) cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
-  else cudaEventRecord(e, s);
+inline void rec_event(cudaEvent_t e, cudaStream_t s) {
+  if (e) cudaEventRecord(e, s);
 }
 
-// Events the timed step graph records: step start, WENO start and r2c end of
-// each stage (the nonlinear bucket), step end.  The others (after WENO, after
-// the rho pass, stage-2 start) are not needed for the buckets, and every
-// event-record node costs a dependency break inside the graph.
-inline bool timed_event_needed(int i, int nev) {
-  const int in_stage = i % EV_PER_STAGE;
-  return i == 0 || i == nev - 1 || in_stage == 1 || in_stage == 3;
+// bucket stamp of a march launch (slots: internal.h StepStamp); slot < 0: none
+inline StepStamp stamp_of(const nwb_plan* p, int slot) {
+  return StepStamp{slot >= 0 ? p->stamps : nullptr, p->step_ctr, slot < 0 ? 0 : slot};
 }
 
 template <typename T>
 void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   cudaStream_t s = p->stream;
-  if (ev) rec_event(p, ev[0], s);
+  if (ev) rec_event(ev[0], s);
   // theta c2r of T (stage 1) or T* (stage 2) into v
   ThetaArgs<T> c = theta_args<T>(p);
   c.spec_in = (const cplx<T>*)(stage == 1 ? p->t : p->ts);
@@ -492,17 +476,20 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
   c.row_off = stage - 1;
   c.alpha_bits = p->red + (stage - 1);
   c.vmax_bits = stage == 1 ? p->vmax_hist : nullptr;
+  c.ts = stamp_of(p, stage == 1 ? 0 : -1);
   launch_theta_c2r<T>(c, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows_c2r, s);
-  if (ev) rec_event(p, ev[1], s);
+  if (ev) rec_event(ev[1], s);
   // WENO -> b
   WenoArgs<T> w = weno_args<T>(p);
   w.step_ctr = p->step_ctr;
   w.row_off = stage - 1;
   w.alpha_bits = p->red + (stage - 1);
+  w.ts = stamp_of(p, stage == 1 ? 1 : 3);
   // theta r2c of b -> bt
   ThetaArgs<T> r = theta_args<T>(p);
   r.phys_in = (const T*)p->b;
   r.spec_out = (cplx<T>*)p->bt;
+  r.ts = stamp_of(p, stage == 1 ? 2 : 4);
   const int nc = p->overlap_chunks;
   if (!ev && nc > 1 && !p->theta_stream_rows) {
     // row chunks of 128-row multiples: WENO(c+1) on `s` overlaps r2c(c) on `side`
@@ -518,15 +505,16 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
       r.row_begin = j;
       r.row_end = je;
       launch_theta_r2c<T>(r, p->theta_rows, p->side);
+      w.ts.buf = r.ts.buf = nullptr;  // the first chunk stamps the bucket
     }
     cudaEventRecord(p->ov_ev[8], p->side);
     cudaStreamWaitEvent(s, p->ov_ev[8], 0);
   } else {
     launch_weno<T>(w, s);
-    if (ev) rec_event(p, ev[2], s);
+    if (ev) rec_event(ev[2], s);
     launch_theta_r2c<T>(r, p->theta_stream_rows ? -p->theta_stream_rows : p->theta_rows, s);
   }
-  if (ev) rec_event(p, ev[3], s);
+  if (ev) rec_event(ev[3], s);
   // rho pass
   RhoArgs<T> q = rho_args<T>(p);
   q.in = (const cplx<T>*)p->bt;
@@ -547,7 +535,7 @@ void launch_stage(nwb_plan* p, int stage, int scheme, cudaEvent_t* ev) {
     q.zero_bits = p->red + 0;
   }
   launch_rho<T>(q, mode, p->rho_threads, s);
-  if (ev) rec_event(p, ev[4], s);
+  if (ev) rec_event(ev[4], s);
 }
 
 // ev (optional): 2 * EV_PER_STAGE events
@@ -559,13 +547,7 @@ template <typename T> void launch_step(nwb_plan* p, int scheme, cudaEvent_t* ev)
 void drop_graphs(nwb_plan* p) {
   for (int i = 0; i < 2; ++i) {
     if (p->graph[i]) cudaGraphExecDestroy(p->graph[i]);
-    for (auto& x : p->tgraph[i]) {
-      if (x) cudaGraphExecDestroy(x);
-      x = nullptr;
-    }
-    if (p->tgraph_g[i]) cudaGraphDestroy(p->tgraph_g[i]);
     p->graph[i] = nullptr;
-    p->tgraph_g[i] = nullptr;
   }
 }
 
@@ -573,10 +555,13 @@ void drop_graphs(nwb_plan* p) {
 int ensure_hist(nwb_plan* p, int len) {
   if (p->hist_len >= len && p->vmax_hist) return NWB_OK;
   dfree(p, p->vmax_hist);
+  dfree(p, p->stamps);
   p->vmax_hist = nullptr;
+  p->stamps = nullptr;
   p->hist_len = len;
   TRY(dalloc(p, (void**)&p->vmax_hist, (size_t)p->g.batch * len * sizeof(u64)));
   CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)p->g.batch * len * sizeof(u64), p->stream));
+  TRY(dalloc(p, (void**)&p->stamps, (size_t)(len + 1) * NWB_TS_SLOTS * sizeof(u64)));
   drop_graphs(p);
   return NWB_OK;
 }
@@ -882,67 +867,6 @@ template <typename T> int graph_for(nwb_plan* p, int scheme) {
   return NWB_OK;
 }
 
-// The timed step graph: launch_step with external event-record nodes at the
-// 2 x EV_PER_STAGE bucket boundaries (placeholder events p->tev); the nodes
-// are kept (in capture order) so march_impl can point them at per-step events.
-template <typename T> int timed_graph_for(nwb_plan* p, int scheme) {
-  const int gi = scheme == NWB_SCHEME_EXPRK22 ? 0 : 1;
-  if (p->tgraph[gi][0] && p->tgraph_stream[gi] == p->stream) return NWB_OK;
-  for (auto& x : p->tgraph[gi]) {
-    if (x) cudaGraphExecDestroy(x);
-    x = nullptr;
-  }
-  if (p->tgraph_g[gi]) cudaGraphDestroy(p->tgraph_g[gi]);
-  p->tgraph_g[gi] = nullptr;
-  for (auto& e : p->tev)
-    if (!e) CU(cudaEventCreate(&e));
-  const int nev_all = (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1) * EV_PER_STAGE;
-  cudaEvent_t cap[10] = {};
-  for (int i = 0; i < nev_all; ++i) cap[i] = timed_event_needed(i, nev_all) ? p->tev[i] : nullptr;
-  cudaGraph_t gr;
-  CU(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-  p->ev_external = true;
-  launch_step<T>(p, scheme, cap);
-  p->ev_external = false;
-  cudaError_t le = cudaGetLastError();
-  CU(cudaStreamEndCapture(p->stream, &gr));
-  if (le != cudaSuccess) {
-    cudaGraphDestroy(gr);
-    return fail(NWB_ECUDA, std::string("timed graph capture: ") + cudaGetErrorString(le));
-  }
-  size_t nn = 0;
-  CU(cudaGraphGetNodes(gr, nullptr, &nn));
-  std::vector<cudaGraphNode_t> nodes(nn);
-  CU(cudaGraphGetNodes(gr, nodes.data(), &nn));
-  const int nev = nev_all;
-  int found = 0, want = 0;
-  for (int i = 0; i < nev; ++i) {
-    p->tnode[gi][i] = nullptr;
-    want += cap[i] != nullptr;
-  }
-  for (auto nd : nodes) {
-    cudaGraphNodeType ty;
-    CU(cudaGraphNodeGetType(nd, &ty));
-    if (ty != cudaGraphNodeTypeEventRecord) continue;
-    cudaEvent_t e;
-    CU(cudaGraphEventRecordNodeGetEvent(nd, &e));
-    for (int i = 0; i < nev; ++i)
-      if (cap[i] && cap[i] == e && !p->tnode[gi][i]) {
-        p->tnode[gi][i] = nd;
-        ++found;
-        break;
-      }
-  }
-  if (found != want) {
-    cudaGraphDestroy(gr);
-    return fail(NWB_ECUDA, "timed graph: event-record nodes not found");
-  }
-  for (auto& x : p->tgraph[gi]) CU(cudaGraphInstantiate(&x, gr, 0));
-  p->tgraph_g[gi] = gr;
-  p->tgraph_stream[gi] = p->stream;
-  return NWB_OK;
-}
-
 template <typename T>
 int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, double max_seconds,
                const int* snap_steps, int n_snap, void* const* snap_bufs, double* max_abs,
@@ -958,31 +882,8 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
   CU(cudaMemsetAsync(p->vmax_hist, 0, (size_t)g.batch * p->hist_len * sizeof(u64), p->stream));
   CU(cudaMemsetAsync(p->red, 0, (size_t)g.batch * 4 * sizeof(u64), p->stream));
   TRY(set_step(p, n0));
-  const int gi = scheme == NWB_SCHEME_EXPRK22 ? 0 : 1;
-  if (step_ms) TRY(timed_graph_for<T>(p, scheme));
-  else TRY(graph_for<T>(p, scheme));
-  const int nev = (scheme == NWB_SCHEME_EXPRK22 ? 2 : 1) * EV_PER_STAGE;
-
-  std::vector<cudaEvent_t> evs;
-  if (step_ms) {
-    evs.resize((size_t)n_steps * 2 * EV_PER_STAGE);
-    for (auto& e : evs) CU(cudaEventCreate(&e));
-  }
-  auto destroy_events = [&]() {
-    // point the timed graphs' event nodes back at the plan's placeholder events
-    // before the per-step events die (a node must never reference a destroyed
-    // event: re-pointing it later fails with cudaErrorInvalidValue)
-    if (step_ms) {
-      cudaStreamSynchronize(p->stream);
-      for (auto ex : p->tgraph[gi])
-        if (ex)
-          for (int q = 0; q < nev; ++q)
-            if (p->tnode[gi][q]) cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], p->tev[q]);
-      cudaGetLastError();
-    }
-    for (auto& e : evs) cudaEventDestroy(e);
-    evs.clear();
-  };
+  // one graph for both modes: the kernels stamp the bucket boundaries (StepStamp)
+  TRY(graph_for<T>(p, scheme));
   const auto t_start = std::chrono::steady_clock::now();
   // budget (max_seconds >= 0; negative = none): checked after every chunk; the
   // first chunk is one step so a zero budget stops after step 1 like the
@@ -999,62 +900,25 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
       int snap = -1;
       for (int q = 0; q < n_snap; ++q)
         if (snap_steps[q] == n) snap = q;
-      if (step_ms && snap >= 0) {
-        cudaEvent_t* ev = &evs[(size_t)(done + i) * 2 * EV_PER_STAGE];
-        launch_stage<T>(p, 1, scheme, ev);
-        cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
-                        cudaMemcpyDeviceToDevice, p->stream);
-        if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, ev + EV_PER_STAGE);
-      } else if (step_ms) {
-        // replay the timed graph with its event nodes pointed at this step's events
-        const int st = done + i;
-        cudaEvent_t* ev = &evs[(size_t)st * 2 * EV_PER_STAGE];
-        cudaGraphExec_t ex = p->tgraph[gi][st % nwb_plan::NTG];
-        cudaError_t e = cudaSuccess;
-        // this instance last ran step st - NTG: wait for it (its last event)
-        // before re-pointing its nodes
-        if (st >= nwb_plan::NTG)
-          e = cudaEventSynchronize(evs[(size_t)(st - nwb_plan::NTG) * 2 * EV_PER_STAGE + nev - 1]);
-        int q = 0;
-        for (; q < nev && e == cudaSuccess; ++q)
-          if (p->tnode[gi][q]) e = cudaGraphExecEventRecordNodeSetEvent(ex, p->tnode[gi][q], ev[q]);
-        const bool set_failed = e != cudaSuccess;
-        if (e == cudaSuccess) e = cudaGraphLaunch(ex, p->stream);
-        if (e != cudaSuccess) {
-          cudaGetLastError();  // do not leave the error for a later launch check
-          destroy_events();
-          return fail(NWB_ECUDA, std::string(set_failed ? "timed graph event node " + std::to_string(q - 1)
-                                                        : std::string("timed graph launch")) +
-                                     " (step " + std::to_string(n) + "): " + cudaGetErrorString(e));
-        }
-      } else if (snap >= 0) {
+      if (snap >= 0) {
         launch_stage<T>(p, 1, scheme, nullptr);
         cudaMemcpyAsync(snap_bufs[snap], p->v, (size_t)g.batch * g.nr * g.nt * sizeof(T),
                         cudaMemcpyDeviceToDevice, p->stream);
         if (scheme == NWB_SCHEME_EXPRK22) launch_stage<T>(p, 2, scheme, nullptr);
       } else {
         cudaError_t e = cudaGraphLaunch(p->graph[scheme == NWB_SCHEME_EXPRK22 ? 0 : 1], p->stream);
-        if (e != cudaSuccess) {
-          destroy_events();
-          return fail(NWB_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
-        }
+        if (e != cudaSuccess) return fail(NWB_ECUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
       }
     }
     cudaError_t le = cudaGetLastError();
-    if (le != cudaSuccess) {
-      destroy_events();
-      return fail(NWB_ECUDA, std::string("march launch: ") + cudaGetErrorString(le));
-    }
+    if (le != cudaSuccess) return fail(NWB_ECUDA, std::string("march launch: ") + cudaGetErrorString(le));
     // guard check on this chunk (host sync)
     hbuf.resize((size_t)g.batch * cnt);
     for (int mbr = 0; mbr < g.batch; ++mbr)
       cudaMemcpyAsync(hbuf.data() + (size_t)mbr * cnt, p->vmax_hist + (size_t)mbr * p->hist_len + n0 + done,
                       cnt * sizeof(u64), cudaMemcpyDeviceToHost, p->stream);
     cudaError_t se = cudaStreamSynchronize(p->stream);
-    if (se != cudaSuccess) {
-      destroy_events();
-      return fail(NWB_ECUDA, std::string("march: ") + cudaGetErrorString(se));
-    }
+    if (se != cudaSuccess) return fail(NWB_ECUDA, std::string("march: ") + cudaGetErrorString(se));
     for (int i = 0; i < cnt && rc == NWB_OK; ++i) {
       for (int mbr = 0; mbr < g.batch; ++mbr) {
         double m;
@@ -1081,20 +945,26 @@ int march_impl(nwb_plan* p, int scheme, int n0, int n_steps, double guard, doubl
       }
     }
   }
-  if (step_ms) {
-    const int ran = done;
-    for (int i = 0; i < ran; ++i) {
-      cudaEvent_t* ev = &evs[(size_t)i * 2 * EV_PER_STAGE];
-      const bool two = scheme == NWB_SCHEME_EXPRK22;
-      float tot = 0, a = 0, b = 0;
-      cudaEventElapsedTime(&tot, ev[0], ev[two ? 2 * EV_PER_STAGE - 1 : EV_PER_STAGE - 1]);
-      cudaEventElapsedTime(&a, ev[1], ev[3]);  // WENO + theta r2c, stage 1
-      if (two) cudaEventElapsedTime(&b, ev[EV_PER_STAGE + 1], ev[EV_PER_STAGE + 3]);
+  if (step_ms && done > 0) {
+    // end stamp of the last step (= slot 0 of step n0 + done), then one read-back
+    launch_stamp(p->stamps, p->step_ctr, 0, p->stream);
+    std::vector<u64> ts((size_t)(done + 1) * NWB_TS_SLOTS);
+    cudaMemcpyAsync(ts.data(), p->stamps + (size_t)n0 * NWB_TS_SLOTS, ts.size() * sizeof(u64),
+                    cudaMemcpyDeviceToHost, p->stream);
+    cudaError_t se = cudaStreamSynchronize(p->stream);
+    if (se != cudaSuccess && rc == NWB_OK)
+      return fail(NWB_ECUDA, std::string("march time stamps: ") + cudaGetErrorString(se));
+    const bool two = scheme == NWB_SCHEME_EXPRK22;
+    auto ms = [](u64 a, u64 b) { return b > a ? (float)((double)(b - a) * 1e-6) : 0.f; };
+    for (int i = 0; i < done; ++i) {
+      const u64* t = &ts[(size_t)i * NWB_TS_SLOTS];
+      const float tot = ms(t[0], t[NWB_TS_SLOTS]);
+      // nonlinear bucket = WENO (b_eval, exprk.py:161-171): WENO start -> r2c start
+      const float nl = std::min(tot, ms(t[1], t[2]) + (two ? ms(t[3], t[4]) : 0.f));
       step_ms[(size_t)i * 3 + 0] = tot;
-      step_ms[(size_t)i * 3 + 1] = a + b;
-      step_ms[(size_t)i * 3 + 2] = tot - (a + b);
+      step_ms[(size_t)i * 3 + 1] = nl;
+      step_ms[(size_t)i * 3 + 2] = tot - nl;
     }
-    destroy_events();
   }
   return rc;
 }
@@ -1882,8 +1752,6 @@ int nwb_plan_destroy(nwb_plan* p) {
   cudaSetDevice(p->device);
   cudaStreamSynchronize(p->stream);
   drop_graphs(p);
-  for (cudaEvent_t e : p->tev)
-    if (e) cudaEventDestroy(e);
   for (void* a : p->allocs)
     if (a) cudaFreeAsync(a, p->stream);
   if (p->own_stream) cudaStreamDestroy(p->own_stream);

@@ -27,6 +27,25 @@ struct Geom {
   int nr, nt, m, kk, ld, batch;
 };
 
+// Per-step bucket time stamps of the march (exprk.py:159-177's nonlinear /
+// linear split): block (0, 0, 0) of a stamped launch writes %globaltimer at
+// entry into buf[*step * NWB_TS_SLOTS + slot] -- slot 0 c2r of stage 1 (step
+// start), 1 / 3 WENO start, 2 / 4 r2c start of stage 1 / 2 (WENO end); the
+// next step's slot 0 ends a step.  No graph nodes, no host work per step.
+constexpr int NWB_TS_SLOTS = 5;
+struct StepStamp {
+  unsigned long long* buf;    // null: no stamp
+  const int* step;
+  int slot;
+};
+__device__ __forceinline__ void step_stamp(const StepStamp& s) {
+  if (s.buf && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    s.buf[(size_t)(*s.step) * NWB_TS_SLOTS + s.slot] = t;
+  }
+}
+
 template <typename T> struct ThetaArgs {
   Geom g;
   FftDesc dh;                 // half-length (m) complex transform
@@ -61,6 +80,7 @@ template <typename T> struct ThetaArgs {
   const cplx<T>* tw_first;
   int ilv;                    // transit layout: 1 = position q msub + i stored at i r1 + q
   int bulk;                   // r2c row loads as TMA bulk copies (fp64 rows)
+  StepStamp ts;               // bucket time stamp at kernel entry (march only)
 };
 
 template <typename T> struct RhoArgs {
@@ -143,8 +163,10 @@ template <typename T> struct WenoArgs {
   // output row chunk [row_begin, row_end) (row_end 0 = all rows; row_begin a
   // multiple of the CTA's 128 rows)
   int row_begin, row_end;
+  StepStamp ts;               // bucket time stamp at kernel entry (march only)
 };
 
+void launch_stamp(unsigned long long* buf, const int* step, int slot, cudaStream_t s);
 template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s);
 template <typename T> void launch_theta_r2c(const ThetaArgs<T>& a, int rows, cudaStream_t s);
 template <typename T> void launch_rho(const RhoArgs<T>& a, int mode, int threads, cudaStream_t s);

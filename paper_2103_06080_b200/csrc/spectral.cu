@@ -200,6 +200,7 @@ __device__ __forceinline__ void split_dit_rows(cplx<T>* z, const ThetaArgs<T>& a
 // SPLIT: the CTA owns rows i + r msub (i = blockIdx.x < msub), else rows j0 + r
 template <typename T, int R, bool SPLIT>
 __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R, SPLIT>())) k_theta_c2r(const ThetaArgs<T> a) {
+  step_stamp(a.ts);
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
@@ -332,6 +333,7 @@ __device__ __forceinline__ void r2c_post_split(const cplx<T>* z, const ThetaArgs
 
 template <typename T, int R, bool SPLIT>
 __global__ void __launch_bounds__(theta_threads<R>(), (theta_min_blocks<T, R, SPLIT>())) k_theta_r2c(const ThetaArgs<T> a) {
+  step_stamp(a.ts);
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* z = reinterpret_cast<V*>(smem_raw);
@@ -408,6 +410,7 @@ __device__ __forceinline__ void c2r_issue(const ThetaArgs<T>& a, cplx<T>* z, int
 
 template <typename T, int R>
 __global__ void __launch_bounds__(512, 1) k_theta_c2r_stream(const ThetaArgs<T> a) {
+  step_stamp(a.ts);
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nr = a.g.nr;
@@ -465,6 +468,7 @@ __device__ __forceinline__ void r2c_issue(const ThetaArgs<T>& a, cplx<T>* z, int
 
 template <typename T, int R>
 __global__ void __launch_bounds__(512, 1) k_theta_r2c_stream(const ThetaArgs<T> a) {
+  step_stamp(a.ts);
   using V = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nr = a.g.nr;

@@ -25,6 +25,14 @@
 
 namespace nwb {
 
+__global__ void k_stamp(unsigned long long* buf, const int* step, int slot) {
+  StepStamp st{buf, step, slot};
+  step_stamp(st);
+}
+void launch_stamp(unsigned long long* buf, const int* step, int slot, cudaStream_t s) {
+  k_stamp<<<1, 32, 0, s>>>(buf, step, slot);
+}
+
 __device__ __forceinline__ double bits_to_real(u64 b) { return __longlong_as_double((long long)b); }
 
 // 1 / b to ~1 ulp: hardware reciprocal seed refined by one cubic step
@@ -149,6 +157,7 @@ constexpr int WTS = WT + 9;
 constexpr int kWalkUnroll = NWB_WENO_WALK_UNROLL;  // walk tile row stride: odd (conflict-free half-warps), >= 38 slots
 template <typename T, int WTR, bool WALK>
 __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoArgs<T> a) {
+  step_stamp(a.ts);
   constexpr int FTS = WALK ? WTS : WT + 1;                // theta-face row stride
   __shared__ T lp[WALK ? 1 : WWARPS][WT + 8], lm[WALK ? 1 : WWARPS][WT + 8];  // split fluxes of one row
   __shared__ T ft[WWARPS][WTR][FTS];                     // theta faces of the tile (WALK: V first)
@@ -418,6 +427,7 @@ constexpr int WT2 = 64;  // columns per warp tile (two per lane)
 constexpr int WTS2 = WT2 + 7;  // walk tile row stride: odd, >= 70 slots
 template <typename T, int WTR, bool WALK>
 __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
+  step_stamp(a.ts);
   using P = typename pair_of<T>::type;
   constexpr int FTS = WALK ? WTS2 : WT2 + 1;
   __shared__ T lp[WALK ? 1 : WWARPS][WT2 + 8], lm[WALK ? 1 : WWARPS][WT2 + 8];  // split fluxes of one row

@@ -329,9 +329,11 @@ def run_exprk22(config: DomainConfig, v0, fields, snapshot_sigmas=None,
     """March to sigma = Sigma on the device (reference ``exprk.py:219-331``).
 
     Extra keywords: ``device`` (CUDA device; default current), ``timing``
-    (default: per-step bucket events recorded by the replayed step graph;
-    ``False`` replays the graph without them and reports the average step
-    time in every slot).
+    (default: per-step buckets from device time stamps the march kernels
+    write -- nonlinear = WENO, linear = the rest, as ``exprk.py:176-177`` --
+    read back once after the march; ``False`` skips the read-back and
+    reports the average step time in every slot).  Both replay the same
+    CUDA graph.
     """
     if scheme not in ("exprk22", "expeuler"):
         raise ValueError(f"unknown scheme {scheme!r}")

@@ -1,7 +1,8 @@
 """GPU: the drop-in march API's host-facing behaviour (reference
 ``nwave/exprk.py:219-331``) -- snapshots streamed to host memory through a
-two-buffer device ring, the per-step timing buckets recorded by the replayed
-step graph, the wall-clock budget and the guard's failure sigma."""
+two-buffer device ring, the per-step timing buckets (device time stamps
+written by the march kernels of the replayed step graph), the wall-clock
+budget and the guard's failure sigma."""
 
 import numpy as np
 import pytest
@@ -69,8 +70,8 @@ def test_many_snapshots_do_not_grow_device_memory(cuda):
 
 
 def test_default_timing_buckets_and_graph_path_agree(cuda):
-    """The default call (per-step buckets from the timed graph) fills the
-    reference's per-step arrays and is bitwise the untimed graph replay."""
+    """The default call (per-step buckets from the kernels' time stamps)
+    fills the reference's per-step arrays and is bitwise the untimed call."""
     c, v0 = _set(1)
     K = 20
     f = nw.zero_fields(K + 2, c.N_rho + 1)
