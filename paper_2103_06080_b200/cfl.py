@@ -52,5 +52,9 @@ def check_cfl_exprk(config: DomainConfig, fields, v_max_bound: float = 5.0) -> C
     elif hasattr(fields.u_perp, "abs"):      # device tensor (device-generated medium)
         u_perp_max = float(fields.u_perp.abs().max())
     else:
-        u_perp_max = float(np.max(np.abs(fields.u_perp)))
+        # max |u| as max(max u, -min u): the same value (NaN and +-inf included)
+        # without np.abs's full-size temporary (C2: 192 MB)
+        u = np.asarray(fields.u_perp)
+        hi, lo = float(np.max(u)), float(np.min(u))
+        u_perp_max = hi if np.isnan(hi) else abs(max(hi, -lo))
     return check_cfl_splitting(config, v_max_bound, u_perp_max)

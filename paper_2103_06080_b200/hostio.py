@@ -15,11 +15,37 @@
 
 from __future__ import annotations
 
+import os
 import threading
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
 STAGE_BYTES = 32 << 20
+
+# host-side copies of a staging chunk run on a few threads: np.copyto releases
+# the GIL, and a fresh destination's first-touch page faults then proceed in
+# parallel (C2 field, 287 MB into np.empty: ~50 ms serial, ~16 ms on 8 threads)
+_COPY_THREADS = max(1, min(8, os.cpu_count() or 1))
+_pool = None
+_pool_lock = threading.Lock()
+
+
+def par_copyto(dst: np.ndarray, src: np.ndarray) -> None:
+    """np.copyto(dst, src, casting="unsafe") for 1-D arrays, split over threads."""
+    global _pool
+    n = dst.size
+    if _COPY_THREADS == 1 or n < (1 << 18):
+        np.copyto(dst, src, casting="unsafe")
+        return
+    with _pool_lock:
+        if _pool is None:
+            _pool = ThreadPoolExecutor(_COPY_THREADS, thread_name_prefix="nwb-copy")
+    step = (n + _COPY_THREADS - 1) // _COPY_THREADS
+    futs = [_pool.submit(np.copyto, dst[a:a + step], src[a:a + step], casting="unsafe")
+            for a in range(0, n, step)]
+    for f in futs:
+        f.result()
 
 _free_pairs: dict = {}  # device index -> list of idle staging pairs
 _staging_lock = threading.Lock()
@@ -70,14 +96,14 @@ def copy_to_host(src, out: np.ndarray, stream=None) -> np.ndarray:
                 if len(pending) == 2:  # buffer k is still held by chunk i-2: drain it
                     ev, kk, s0, e0 = pending.pop(0)
                     ev.synchronize()
-                    np.copyto(dst[s0:e0], views[kk][: e0 - s0].numpy(), casting="unsafe")
+                    par_copyto(dst[s0:e0], views[kk][: e0 - s0].numpy())
                 views[k][: e - s].copy_(flat[s:e], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(stream)
                 pending.append((ev, k, s, e))
             for ev, kk, s0, e0 in pending:
                 ev.synchronize()
-                np.copyto(dst[s0:e0], views[kk][: e0 - s0].numpy(), casting="unsafe")
+                par_copyto(dst[s0:e0], views[kk][: e0 - s0].numpy())
     finally:
         _release_pair(src.device.index, bufs)
     return out

@@ -16,6 +16,7 @@ import numpy as np
 from . import _lib
 from ._lib import check, ptr
 from .errors import InstabilityError
+from .hostio import par_copyto
 
 _STAGE_BYTES = 32 << 20  # page-locked staging chunk for large host -> device copies
 
@@ -107,7 +108,8 @@ class DevicePlan:
         torch = _torch()
         if isinstance(arr, torch.Tensor):
             return arr.to(device=self.device, dtype=dtype).contiguous()
-        host = torch.from_numpy(np.ascontiguousarray(arr))
+        host_np = np.ascontiguousarray(arr)
+        host = torch.from_numpy(host_np)
         if host.numel() * host.element_size() < 2 * _STAGE_BYTES:
             return host.to(device=self.device, dtype=dtype, non_blocking=False).contiguous()
         # large host arrays (a C2 field is 287 MB): through two page-locked staging
@@ -116,6 +118,7 @@ class DevicePlan:
         # ~11 GB/s
         out = torch.empty(tuple(host.shape), dtype=dtype, device=self.device)
         src, dst = host.reshape(-1), out.reshape(-1)
+        src_np = host_np.reshape(-1)
         per = _STAGE_BYTES // max(src.element_size(), out.element_size())
         bufs = [torch.empty(per, dtype=dtype, pin_memory=True) for _ in range(2)]
         done = [None, None]
@@ -124,7 +127,7 @@ class DevicePlan:
             e, k = min(src.numel(), s + per), i & 1
             if done[k] is not None:
                 done[k].synchronize()
-            bufs[k][: e - s].copy_(src[s:e])
+            par_copyto(bufs[k][: e - s].numpy(), src_np[s:e])
             dst[s:e].copy_(bufs[k][: e - s], non_blocking=True)
             done[k] = torch.cuda.Event()
             done[k].record(stream)

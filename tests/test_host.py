@@ -258,3 +258,29 @@ def test_symmetric_table_position_map(stages):
         if p >= m:
             assert _sym_pos(pos_of[(n - freq[p]) % n], stages[0], m) == c
     assert len(canon) <= n // 2 + m + 1
+
+
+def test_par_copyto_matches_copyto():
+    """The threaded host copy used by the staged transfers: same bytes as
+    np.copyto, including the fp64 -> fp32 narrowing of fp32 plans."""
+    from paper_2103_06080_b200.hostio import par_copyto
+
+    rng = np.random.default_rng(7)
+    src = rng.standard_normal(1_000_003)
+    for dt in (np.float64, np.float32):
+        a, b = np.empty(src.size, dt), np.empty(src.size, dt)
+        par_copyto(a, src)
+        np.copyto(b, src, casting="unsafe")
+        assert np.array_equal(a, b)
+
+
+def test_cfl_u_perp_max_without_abs_temporary():
+    """max(max u, -min u) reproduces max|u| bit for bit (NaN, inf, -0.0)."""
+    from paper_2103_06080_b200.cfl import check_cfl_exprk
+
+    c = nw.preset_config(1)
+    for arr in ([[1.0, -3.0]], [[-3.0, -1.0]], [[np.nan, 1.0]], [[1.0, np.nan]],
+                [[-np.inf, 1.0]], [[-0.0, -0.0]]):
+        a = np.array(arr)
+        f = nw.VelocityFields(a, a, a, a)
+        assert repr(check_cfl_exprk(c, f).u_perp_max) == repr(float(np.max(np.abs(a))))
