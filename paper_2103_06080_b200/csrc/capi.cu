@@ -293,6 +293,9 @@ struct nwb_plan {
   int rho_persistent = 0;    // persistent streaming rho pass (NWB_RHO_PERSIST=1 enables; measured slower)
   int rho_ws = 0, rho_ws2 = 0, rho_ws_ctas = 0;  // warp-specialised rho pass (k_rho_ws) group sizes, CTAs
   void* ws_scratch = nullptr;
+  // WENO walk tiles staged by TMA (fp64): tiled tensor map over v (NWB_WENO_TMA=0: cp.async)
+  int weno_tma = 0;
+  alignas(64) CUtensorMap vmap;
   // first rho stage fused into the theta passes (r1 > 1): rho CTAs own
   // msub = nr / r1 point sub-columns (dsub / tw_sub); tw_first = W_nr^t
   int rho_r1 = 1, msub = 0, ilv = 1;
@@ -447,6 +450,8 @@ template <typename T> WenoArgs<T> weno_args(const nwb_plan* p) {
   a.bcoef = (T)p->B;
   a.inv_drho = (T)(1.0 / (p->rho_span / p->g.nr));
   a.inv_dtheta = (T)(1.0 / (p->theta_span / p->g.nt));
+  a.tma = p->weno_tma;
+  if (p->weno_tma) a.vmap = p->vmap;
   return a;
 }
 
@@ -578,6 +583,41 @@ int check_plan(nwb_plan* p) {
   return NWB_OK;
 }
 
+// Tiled tensor map over an fp64 field (nt columns, nr rows, batch members) whose
+// box is one WENO walk tile (WENO_TMA_BOX x 32 x 1).  cuTensorMapEncodeTiled
+// comes from the driver through the runtime's entry-point query, so the library
+// links against cudart only.  Returns 1 when the map is usable (row pitch a
+// multiple of 16 bytes, grid at least one tile), else 0: cp.async staging.
+int make_weno_vmap(CUtensorMap& map, const void* v, int nt, int nr, int batch) {
+  if (const char* env = std::getenv("NWB_WENO_TMA"))  // measurement knob
+    if (env[0] == '0') return 0;
+  if (nt % 2 || nt < 64 || nr < 32 || ((uintptr_t)v & 15)) return 0;
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+      cudaGetLastError();
+      return 0;
+    }
+    encode = (EncodeFn)fn;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)nt, (cuuint64_t)nr, (cuuint64_t)batch};
+  const cuuint64_t strides[2] = {(cuuint64_t)nt * 8, (cuuint64_t)nt * nr * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)WENO_TMA_BOX, 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(v), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
 template <typename T> int create_impl(nwb_plan* p) {
   const Geom& g = p->g;
   const size_t C = sizeof(cplx<T>);
@@ -591,6 +631,7 @@ template <typename T> int create_impl(nwb_plan* p) {
   TRY(dalloc(p, &p->bt, spec));
   TRY(dalloc(p, &p->v, phys));
   TRY(dalloc(p, &p->b, phys));
+  if (sizeof(T) == 8) p->weno_tma = make_weno_vmap(p->vmap, p->v, g.nt, g.nr, g.batch);
   TRY(dalloc(p, &p->E, tab));
   TRY(dalloc(p, &p->P1, tab));
   TRY(dalloc(p, &p->P12, tab));
@@ -837,6 +878,8 @@ template <typename T> int weno_impl(const Geom& g, const void* v, const void* up
   w.bcoef = (T)b;
   w.inv_drho = (T)(1.0 / d_rho);
   w.inv_dtheta = (T)(1.0 / d_theta);
+  if (sizeof(T) == 8) w.tma = make_weno_vmap(w.vmap, v, g.nt, g.nr, g.batch);
+
   launch_weno<T>(w, s);
   CHECK_LAUNCH("weno5_b");
   return NWB_OK;

@@ -1,6 +1,7 @@
 // Shared device helpers: complex arithmetic on double2/float2, ordered-bit
 // max reductions, launch checking.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -145,6 +146,22 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned 
 }
 __device__ __forceinline__ void bulk_commit_wait_read() {
   asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+// make an mbarrier's initialisation visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+// TMA tiled load of one box of a rank-3 tensor map (coordinates innermost
+// first, signed: out-of-bounds elements are zero-filled) completing the box's
+// bytes on the mbarrier (SASS UTMALDG); `map` must live in param / const /
+// global memory (a __grid_constant__ kernel parameter)
+__device__ __forceinline__ void tma_load_3d(void* sdst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(sdst)),
+      "l"((unsigned long long)(uintptr_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -164,7 +164,14 @@ template <typename T> struct WenoArgs {
   // multiple of the CTA's 128 rows)
   int row_begin, row_end;
   StepStamp ts;               // bucket time stamp at kernel entry (march only)
+  // TMA staging of the walk tiles (fp64, plain mode): rank-3 tiled map over v
+  // (columns, rows, members), box WENO_TMA_BOX x 32 x 1; tma = 0: cp.async
+  int tma;
+  alignas(64) CUtensorMap vmap;
 };
+// TMA box width: columns x0-4 .. x0+37 (the inner start coordinate of a tiled
+// copy must be 16-byte aligned: x0-3 is not, x0-4 is); 336 B rows
+constexpr int WENO_TMA_BOX = 42;
 
 void launch_stamp(unsigned long long* buf, const int* step, int slot, cudaStream_t s);
 template <typename T> void launch_theta_c2r(const ThetaArgs<T>& a, int rows, cudaStream_t s);

@@ -155,12 +155,22 @@ constexpr int WTS = WT + 9;
 #define NWB_WENO_WALK_UNROLL 6
 #endif
 constexpr int kWalkUnroll = NWB_WENO_WALK_UNROLL;  // walk tile row stride: odd (conflict-free half-warps), >= 38 slots
-template <typename T, int WTR, bool WALK>
-__global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoArgs<T> a) {
+//
+// TMA (fp64 walk, plain mode): the warp's V tile arrives as ONE tensor copy
+// issued by lane 0 -- box columns x0-4 .. x0+37 (a tiled copy's inner start
+// must be 16-byte aligned, so the box starts one column before the halo) of
+// rows j0 .. j0+31, zero-filled outside the grid; tiles touching the periodic
+// seam patch the wrapped columns with plain loads -- instead of ~38 cp.async
+// per lane.  The dense box sets the row stride to 42 (2-way bank conflicts in
+// the walk instead of none) and slot s of the cp.async layout sits at s + 1.
+template <typename T, int WTR, bool WALK, bool TMA>
+__global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __grid_constant__ WenoArgs<T> a) {
   step_stamp(a.ts);
-  constexpr int FTS = WALK ? WTS : WT + 1;                // theta-face row stride
+  static_assert(!TMA || (WALK && WTR == WT), "TMA staging is a walk-tile path");
+  constexpr int FTS = TMA ? WENO_TMA_BOX : WALK ? WTS : WT + 1;  // theta-face row stride
   __shared__ T lp[WALK ? 1 : WWARPS][WT + 8], lm[WALK ? 1 : WWARPS][WT + 8];  // split fluxes of one row
-  __shared__ T ft[WWARPS][WTR][FTS];                     // theta faces of the tile (WALK: V first)
+  __shared__ __align__(128) T ft[WWARPS][WTR][FTS];      // theta faces of the tile (WALK: V first)
+  __shared__ __align__(8) unsigned long long tbar[TMA ? WWARPS : 1];
   const int nr = a.g.nr, nt = a.g.nt;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mem = blockIdx.z;
@@ -194,6 +204,27 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
 
   if constexpr (WALK) {
     // ---- theta faces, lane r walks row r: stage the tile's V (slot s = column x0 + s - 3)
+    if constexpr (TMA) {
+      unsigned long long* bar = &tbar[w];
+      if (lane == 0) {
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, (unsigned)(WENO_TMA_BOX * WT * sizeof(T)));
+        tma_load_3d(&ftw[0][0], &a.vmap, x0 - 4, halo ? j0 + 3 : j0, mem, bar);
+      }
+      mbar_wait(bar, 0);
+      if (x0 < 3 || x0 + 35 > nt) {  // warp-uniform: the tile touches the seam
+        // box slots 1 .. 38 hold columns x0-3 .. x0+34; lane patches slot lane + 1
+        // and (lanes < 6) slot lane + 33 when its column lies outside [0, nt)
+        const bool lo_w = (unsigned)(x0 + lane - 3) >= (unsigned)nt;
+        const bool hi_w = lane < 6 && x0 + lane + 29 >= nt;
+        for (int r = 0; r < rows; ++r) {
+          const T* vr = v + (size_t)vrow(j0 + r) * nt;
+          if (lo_w) ftw[r][lane + 1] = vr[kl];
+          if (hi_w) ftw[r][33 + lane] = vr[kh];
+        }
+      }
+    } else {
 #if NWB_WENO_CPASYNC
     // as asynchronous copies: all of the lane's 32-38 loads in flight at once,
     // no register round trip (the staging stalled on each batch of loads)
@@ -211,11 +242,12 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
       if (lane < 6) ftw[r][32 + lane] = vr[kh];
     }
 #endif
+    }  // !TMA
     __syncwarp();
     if (lane < rows) {
       const T c = mul_rn(pi, upar[j0 + lane]);
       const T cp = hath - c, cm = -hath - c;
-      T* tr = ftw[lane];
+      T* tr = ftw[lane] + (TMA ? 1 : 0);
       // p / m: split fluxes at window slots 0..5; dp[s] = dsq(p[s-1], p[s], p[s+1]),
       // dm[s] = dsq(m[s+1], m[s], m[s-1]) (the argument orders of face_pair)
       T p[6], m[6], dp[6], dm[6];
@@ -314,7 +346,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const WenoA
   // output / du pointers of row j0 (advanced one row per face after the first)
   T* outp = a.out + (size_t)mem * nr * nt + (size_t)j0 * nt + (col_ok ? k : 0);
   const T* dup = du + j0;
-  const T* ftp = &ftw[0][lane];
+  const T* ftp = &ftw[0][lane + (TMA ? 1 : 0)];
   // fp64 faces come as 6 F (face_pair_d)
   const T idth = sizeof(T) == 8 ? a.inv_dtheta * (T)(1.0 / 6.0) : a.inv_dtheta;
   const T idrh = sizeof(T) == 8 ? a.inv_drho * (T)(1.0 / 6.0) : a.inv_drho;
@@ -426,7 +458,7 @@ constexpr int WT2 = 64;  // columns per warp tile (two per lane)
 // lane y has already overwritten) is a discarded duplicate.
 constexpr int WTS2 = WT2 + 7;  // walk tile row stride: odd, >= 70 slots
 template <typename T, int WTR, bool WALK>
-__global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const WenoArgs<T> a) {
+__global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__ WenoArgs<T> a) {
   step_stamp(a.ts);
   using P = typename pair_of<T>::type;
   constexpr int FTS = WALK ? WTS2 : WT2 + 1;
@@ -716,8 +748,14 @@ template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, c
     }
   }
   dim3 grid((a.g.nt + WT - 1) / WT, gy, a.g.batch);
-  if (WTR == 32 && weno_walk()) k_weno<T, WTR, true><<<grid, WWARPS * 32, 0, s>>>(a);
-  else k_weno<T, WTR, false><<<grid, WWARPS * 32, 0, s>>>(a);
+  if constexpr (sizeof(T) == 8 && WTR == 32) {
+    if (a.tma && weno_walk()) {
+      k_weno<T, WTR, true, true><<<grid, WWARPS * 32, 0, s>>>(a);
+      return;
+    }
+  }
+  if (WTR == 32 && weno_walk()) k_weno<T, WTR, true, false><<<grid, WWARPS * 32, 0, s>>>(a);
+  else k_weno<T, WTR, false, false><<<grid, WWARPS * 32, 0, s>>>(a);
 }
 
 // rows per warp tile: 32 unless the grid has fewer than ~2048 tiles (small

@@ -479,6 +479,39 @@ def test_weno_theta_walk_bitwise(cuda, monkeypatch, n_rho, n_theta, batch, preci
         assert np.array_equal(b_ops[0], b_ops[1])
 
 
+@pytest.mark.parametrize("n_rho,n_theta,batch", [
+    (2048, 1024, 1), (2025, 1050, 1), (1050, 2100, 1), (512, 1024, 4), (1000, 448, 5)])
+def test_weno_tma_staging_bitwise(cuda, monkeypatch, n_rho, n_theta, batch):
+    """fp64 walk tiles staged by one TMA tensor copy per warp (zero-filled box,
+    periodic seam patched; NWB_WENO_TMA=0 selects the cp.async staging) hold the
+    same operands: the march and the WENO operator alone are bitwise identical,
+    including grids whose theta extent is not a multiple of the 32-column tile."""
+    from paper_2103_06080_b200.plan import DevicePlan
+
+    cfg = nw.DomainConfig(N_rho=n_rho, N_theta=n_theta, N_sigma=3, Sigma=1.2)
+    _, rho, theta = nw.build_axes(cfg)
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B)).values
+    if batch > 1:
+        v0 = np.stack([v0 * (1.0 + 0.1 * i) for i in range(batch)])
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal((n_rho, n_theta))
+    up, uq, du = (0.03 * rng.standard_normal(n_rho) for _ in range(3))
+    b_ops, outs = [], []
+    for tma in ("0", "1"):
+        monkeypatch.setenv("NWB_WENO_TMA", tma)
+        plan = DevicePlan(n_rho, n_theta, batch, "double", cfg.d_sigma, cfg.rho_span,
+                          cfg.theta_span, cfg.A, cfg.B, nw.EPS_DOUBLE)
+        plan.set_coeffs(None, None, None, n_rows=8)
+        plan.load_physical(v0)
+        plan.march("exprk22", 0, 3)
+        out, _ = plan.store_physical()
+        outs.append(out.cpu().numpy())
+        plan.close()
+        b_ops.append(np.asarray(nw.weno5_b(v, up, uq, du, 0.05, 0.32, 0.21)))
+    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(b_ops[0], b_ops[1])
+
+
 @pytest.mark.parametrize("precision", ["double", "single"])
 def test_large_host_load_staged_equals_device_load(cuda, precision):
     """Host arrays above 64 MB go through the page-locked staging chunks of
