@@ -1210,6 +1210,8 @@ template <typename T> int slab_weno_impl(nwb_slab* s, const void* v_ext, void* b
   w.coef_j0 = s->j0;
   w.nr_glob = s->nr;
   w.halo = 1;
+  // TMA-staged tiles over the slab's rows plus the 3 + 3 halo rows (fp64)
+  if (sizeof(T) == 8) w.tma = make_weno_vmap(w.vmap, v_ext, s->nt, s->rows + 6, 1);
   launch_weno<T>(w, s->stream);
   CHECK_LAUNCH("slab weno");
   return NWB_OK;

@@ -46,6 +46,26 @@ def test_slab_c5_geometry_truncated(cuda, oracle):
     assert max_relative(ref.final, rows.cpu().numpy()) <= 1e-10
 
 
+def test_slab_tma_staging_bitwise(cuda, monkeypatch):
+    """The halo-extended slab WENO stages its fp64 tiles by TMA (rows + 6 halo
+    rows in the tensor map); NWB_WENO_TMA=0 selects cp.async: bitwise equal."""
+    from paper_2103_06080_b200.slab import SlabMarch
+
+    cfg = nw.DomainConfig(Sigma=2.4, N_sigma=6, N_rho=1050, N_theta=2100)
+    _, rho, theta = nw.build_axes(cfg)
+    v0 = nw.rho_modulated(cfg, nw.initial_nwave(rho, theta, cfg.A, cfg.B)).values
+    f = nw.zero_fields(4, cfg.N_rho + 1)
+    outs = []
+    for tma in ("0", "1"):
+        monkeypatch.setenv("NWB_WENO_TMA", tma)
+        sm = SlabMarch(cfg, f, max_steps=2)
+        sm.load(v0)
+        sm.march()
+        rows, _ = sm.final_rows()
+        outs.append(rows.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
 class _ThreadComm:
     """Collectives between virtual ranks that are host threads of one process
     (each with its own slab plan and stream on the one GPU).  Data moves by
