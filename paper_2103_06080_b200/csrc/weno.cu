@@ -358,30 +358,21 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
   // offset / coefficient row of the prefetched row: they advance by one row
   // per iteration, so the periodic wrap is a compare instead of a modulus.
   const T* vcol = v + kv;
-  const int vwrap = (halo ? nr + 6 : nr) * nt;
+  const int vrows = halo ? nr + 6 : nr;
   int ov = vrow(j0 + 2) * nt, ju = wrap_idx(cj0 + j0 + 2, ng);
   T vnext = vcol[ov];
   T unext = uperp_g[ju];
-#pragma unroll 6
-  for (int r = 0; r <= rows; ++r) {
-    // row j0 + r + 2 into window slot 5
-    const T vv = vnext, uu = unext;
-    if (r < rows) {
-      ov += nt;
-      ov = ov == vwrap ? 0 : ov;
-      ju = ju + 1 == ng ? 0 : ju + 1;
-      vnext = vcol[ov];
-      unext = uperp_g[ju];
-    }
+  // one row of the sweep: v / u_perp of row j0 + r + 2 into window slot 5, the
+  // face between rows j0+r-1 and j0+r, and (emit) the output of row j0+r-1
+  auto row_step = [&](const T vv, const T uu, const bool emit) {
     hp[5] = vv * fma(half, uu, harh);
     hm[5] = vv * fma(half, uu, -harh);
     vw[5] = vv;
     dp[3] = dsq(hp[2], hp[3], hp[4]);
     dm[4] = dsq(hm[3], hm[4], hm[5]);
-    // face between rows j0+r-1 and j0+r
     const T f = face_pair_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
                             hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
-    if (r > 0) {
+    if (emit) {
       if (col_ok) {
         const T dth = (ftp[1] - ftp[0]) * idth;
         const T drh = (f - fprev) * idrh;
@@ -399,6 +390,47 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
       vw[d] = vw[d + 1];
       dp[d] = dp[d + 1];
       dm[d] = dm[d + 1];
+    }
+  };
+  // Interior tiles (warp-uniform): every row the sweep prefetches, up to
+  // j0 + rows + 3, lies inside the field and the coefficient row without
+  // wrapping, so the prefetch runs unconditionally on plain pointer increments
+  // (the last one is unused); tiles at the periodic rho seam keep the wrapped
+  // running offsets.  Same operands in the same order either way.
+  const int top = j0 + rows + 3;
+  if ((halo ? top + 3 : top) < vrows && cj0 + top < ng) {
+    const T* vp = vcol + ov;
+    const T* up = uperp_g + ju;
+    {
+      const T vv = vnext, uu = unext;
+      vp += nt;
+      ++up;
+      vnext = *vp;
+      unext = *up;
+      row_step(vv, uu, false);
+    }
+#pragma unroll 6
+    for (int r = 1; r <= rows; ++r) {
+      const T vv = vnext, uu = unext;
+      vp += nt;
+      ++up;
+      vnext = *vp;
+      unext = *up;
+      row_step(vv, uu, true);
+    }
+  } else {
+    const int vwrap = vrows * nt;
+#pragma unroll 6
+    for (int r = 0; r <= rows; ++r) {
+      const T vv = vnext, uu = unext;
+      if (r < rows) {
+        ov += nt;
+        ov = ov == vwrap ? 0 : ov;
+        ju = ju + 1 == ng ? 0 : ju + 1;
+        vnext = vcol[ov];
+        unext = uperp_g[ju];
+      }
+      row_step(vv, uu, r > 0);
     }
   }
 }
