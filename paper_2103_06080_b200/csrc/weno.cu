@@ -662,21 +662,11 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
   const P idth(a.inv_dtheta), idrh(a.inv_drho);
   const T* vc0 = v + kv0;
   const T* vc1 = v + kv1;
-  const int vwrap = (halo ? nr + 6 : nr) * nt;
+  const int vrows = halo ? nr + 6 : nr;
   int ov = vrow(j0 + 2) * nt, ju = wrap_idx(cj0 + j0 + 2, ng);
   P vnext(vc0[ov], vc1[ov]);
   T unext = uperp_g[ju];
-#pragma unroll 4
-  for (int r = 0; r <= rows; ++r) {
-    const P vv = vnext;
-    const T uu = unext;
-    if (r < rows) {
-      ov += nt;
-      ov = ov == vwrap ? 0 : ov;
-      ju = ju + 1 == ng ? 0 : ju + 1;
-      vnext = P(vc0[ov], vc1[ov]);
-      unext = uperp_g[ju];
-    }
+  auto row_step = [&](const P vv, const T uu, const bool emit) {
     hp[5] = vv * P(fma(half, uu, harh));
     hm[5] = vv * P(fma(half, uu, -harh));
     vw[5] = vv;
@@ -684,7 +674,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
     dm[4] = dsq(hm[3], hm[4], hm[5]);
     const P f = face_pair2_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
                               hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
-    if (r > 0) {
+    if (emit) {
       const P dth = (P(ftp[fx1], ftp[fy1]) - P(ftp[0], ftp[fy0])) * idth;
       const P drh = (f - fprev) * idrh;
       const P o = (P(*dup) * vw[2] - dth) - drh;
@@ -702,6 +692,49 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
       vw[d] = vw[d + 1];
       dp[d] = dp[d + 1];
       dm[d] = dm[d + 1];
+    }
+  };
+  // interior tiles: unconditional prefetch on pointer increments (k_weno)
+  const int top = j0 + rows + 3;
+  if ((halo ? top + 3 : top) < vrows && cj0 + top < ng) {
+    const T* vp0 = vc0 + ov;
+    const T* vp1 = vc1 + ov;
+    const T* up = uperp_g + ju;
+    {
+      const P vv = vnext;
+      const T uu = unext;
+      vp0 += nt;
+      vp1 += nt;
+      ++up;
+      vnext = P(*vp0, *vp1);
+      unext = *up;
+      row_step(vv, uu, false);
+    }
+#pragma unroll 4
+    for (int r = 1; r <= rows; ++r) {
+      const P vv = vnext;
+      const T uu = unext;
+      vp0 += nt;
+      vp1 += nt;
+      ++up;
+      vnext = P(*vp0, *vp1);
+      unext = *up;
+      row_step(vv, uu, true);
+    }
+  } else {
+    const int vwrap = vrows * nt;
+#pragma unroll 4
+    for (int r = 0; r <= rows; ++r) {
+      const P vv = vnext;
+      const T uu = unext;
+      if (r < rows) {
+        ov += nt;
+        ov = ov == vwrap ? 0 : ov;
+        ju = ju + 1 == ng ? 0 : ju + 1;
+        vnext = P(vc0[ov], vc1[ov]);
+        unext = uperp_g[ju];
+      }
+      row_step(vv, uu, r > 0);
     }
   }
 }
