@@ -253,6 +253,20 @@ def algorithmic_bytes(cfg, precision: str, batch: int = 1, design: bool = False)
     return [c2r, weno, r2c, rho1, c2r, weno, r2c, rho2]
 
 
+WENO_FLOP_PER_CELL = 287
+FP_PEAKS_FILE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "fp_peaks.json")
+
+
+def fp_peak(precision):
+    """Measured FMA peak (TFLOP/s) of the pipe WENO runs on, or None."""
+    try:
+        with open(FP_PEAKS_FILE) as fh:
+            d = json.load(fh)
+        return float(d["fp64_dfma_tflops" if precision == "double" else "fp32_ffma2_tflops"])
+    except Exception:
+        return None
+
+
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as fh:
@@ -283,6 +297,14 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
                     "GBs": round(abytes[i] / (ms * 1e-3) / 1e9, 1),
                     "frac": round(abytes[i] / (ms * 1e-3) / 1e9 / peak, 4),
                     "design_bytes": dbytes[i]})
+    # WENO is arithmetic-bound: its roofline is the measured FP64 DFMA (fp64) or
+    # packed-FP32 FFMA2 (fp32) peak (profiles/fp_peaks.json, tools/fp_peak.cu), on
+    # the reference's 287 flop per cell
+    fpk = fp_peak(precision)
+    for p in per:
+        if p["kernel"] == "weno" and fpk:
+            tf = WENO_FLOP_PER_CELL * cfg.N_rho * cfg.N_theta * batch / (p["ms"] * 1e-3) / 1e12
+            p.update({"TFLOPs": round(tf, 2), "fp_peak_TFLOPs": fpk, "frac_fp": round(tf / fpk, 4)})
     # dominant kernel type by summed time over the step
     by_kernel = {}
     for p in per:
@@ -310,6 +332,14 @@ def roofline_block(cfg, cname, precision, kernel_ms_total, n_prof, batch=1):
            "share_of_step": round(by_kernel[dom]["ms"] / step_ms, 4),
            "step_frac_16F": None,
            "per_kernel": per}
+    wk = [p for p in per if "frac_fp" in p]
+    if wk:
+        tf = sum(p["TFLOPs"] for p in wk) / len(wk)
+        blk["weno_fp_roofline"] = {
+            "bound": "fp64_dfma" if precision == "double" else "fp32_ffma2", "kernel": "weno",
+            "achieved": round(tf, 2), "peak": fpk, "unit": "TFLOP/s", "frac": round(tf / fpk, 4),
+            "flop_basis": f"{WENO_FLOP_PER_CELL} flop per cell (the reference's count, SURVEY 8(d)); "
+                          "peak measured by tools/fp_peak.cu (profiles/fp_peaks.json)"}
     if dom == "weno":
         # WENO moves 2F per launch but is arithmetic-bound (no tensor-core form):
         # its limiter is the FP64 pipe (fp64) / the FMA-pipe issue rate (fp32),
