@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
 #if NWB_WENO_CPASYNC
     // as asynchronous copies: all of the lane's 32-38 loads in flight at once,
     // no register round trip (the staging stalled on each batch of loads)
-    for (int r = 0; r < rows; ++r) {
-      const T* vr = v + (size_t)vrow(j0 + r) * nt;
+    const T* vr = v + (size_t)(halo ? j0 + 3 : j0) * nt;  // rows j0 .. j0+rows-1 never wrap
+    for (int r = 0; r < rows; ++r, vr += nt) {
       cp_async_real(&ftw[r][lane], vr + kl);
       if (lane < 6) cp_async_real(&ftw[r][32 + lane], vr + kh);
     }
@@ -531,8 +531,10 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
 
   if constexpr (WALK) {
 #if NWB_WENO_CPASYNC
-    for (int r = 0; r < rows; ++r) {
-      const T* vr = v + (size_t)vrow(j0 + r) * nt;
+    // the tile's own rows j0 .. j0+rows-1 never wrap (rows <= jend - j0): a
+    // running row pointer instead of a wrapped row index per row
+    const T* vr = v + (size_t)(halo ? j0 + 3 : j0) * nt;
+    for (int r = 0; r < rows; ++r, vr += nt) {
       cp_async_real(&ftw[r][lane], vr + kl0);
       cp_async_real(&ftw[r][lane + 32], vr + kl1);
       if (lane < 6) cp_async_real(&ftw[r][64 + lane], vr + kh);
