@@ -134,6 +134,25 @@ __device__ __forceinline__ int wrap_idx(int x, int n) {
 constexpr int WT = 32;      // tile edge (cells) per warp
 constexpr int WWARPS = 4;   // warps per CTA, stacked along rho
 
+// unroll of the rho sweeps (measurement knobs): the interior loop of k_weno
+// (6 = the register window's period, no moves) and the rare seam loop (tiles
+// whose prefetch wraps; kept small so the two copies of the sweep do not crowd
+// the instruction cache)
+#ifndef NWB_WENO_SWEEP_UNROLL
+#define NWB_WENO_SWEEP_UNROLL 6
+#endif
+#ifndef NWB_WENO_SEAM_UNROLL
+#define NWB_WENO_SEAM_UNROLL 1
+#endif
+// narrow fields (N_theta < 1024, e.g. the C4 members) run the interior sweep
+// at a smaller unroll: their tiles take the seam / TMA-patch paths more often
+// and the smaller kernel keeps those in the instruction cache (C4 fp64 WENO
+// 1.587 -> 1.506 ms at unroll 3, fp32 0.923 -> 0.873 at 2; C2 prefers 6 / 4)
+constexpr int kSweepUnrollNarrow = 3, kX2UnrollNarrow = 2, kNarrowNt = 1024;
+#define NWB_PRAGMA_(x) _Pragma(#x)
+#define NWB_PRAGMA(x) NWB_PRAGMA_(x)
+#define NWB_SEAM_UNROLL_PRAGMA NWB_PRAGMA(unroll NWB_WENO_SEAM_UNROLL)
+
 // four CTAs (16 warps) per SM: caps the fp64 walk kernels at 128 registers (the
 // TMA-staged one would take 146 and fit three; 124 with no spills measures
 // 0.385 -> 0.378 ms at C2); the other instantiations already fit
@@ -166,7 +185,7 @@ constexpr int kWalkUnroll = NWB_WENO_WALK_UNROLL;  // walk tile row stride: odd 
 // seam patch the wrapped columns with plain loads -- instead of ~38 cp.async
 // per lane.  The dense box sets the row stride to 42 (2-way bank conflicts in
 // the walk instead of none) and slot s of the cp.async layout sits at s + 1.
-template <typename T, int WTR, bool WALK, bool TMA>
+template <typename T, int WTR, bool WALK, bool TMA, int SU = NWB_WENO_SWEEP_UNROLL>
 __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __grid_constant__ WenoArgs<T> a) {
   step_stamp(a.ts);
   static_assert(!TMA || (WALK && WTR == WT), "TMA staging is a walk-tile path");
@@ -409,7 +428,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
       unext = *up;
       row_step(vv, uu, false);
     }
-#pragma unroll 6
+#pragma unroll SU
     for (int r = 1; r <= rows; ++r) {
       const T vv = vnext, uu = unext;
       vp += nt;
@@ -420,7 +439,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
     }
   } else {
     const int vwrap = vrows * nt;
-#pragma unroll 6
+NWB_SEAM_UNROLL_PRAGMA
     for (int r = 0; r <= rows; ++r) {
       const T vv = vnext, uu = unext;
       if (r < rows) {
@@ -484,6 +503,9 @@ __device__ __forceinline__ P face_pair2_d(P p0, P p1, P p2, P p3, P p4, P Dp0, P
 }
 
 constexpr int WT2 = 64;  // columns per warp tile (two per lane)
+#ifndef NWB_WENO_X2_UNROLL
+#define NWB_WENO_X2_UNROLL 4
+#endif
 
 // WALK (32-row tiles): lane r walks row r of the staged 32 x 70 V tile, the two
 // halves packed -- faces 0..32 from slots 0..37 (lane x) and faces 32..64 from
@@ -492,7 +514,7 @@ constexpr int WT2 = 64;  // columns per warp tile (two per lane)
 // after slot g + 5 is read); lane x's face 32 (its last, whose newest slot 37
 // lane y has already overwritten) is a discarded duplicate.
 constexpr int WTS2 = WT2 + 7;  // walk tile row stride: odd, >= 70 slots
-template <typename T, int WTR, bool WALK>
+template <typename T, int WTR, bool WALK, int SU = NWB_WENO_X2_UNROLL>
 __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__ WenoArgs<T> a) {
   step_stamp(a.ts);
   using P = typename pair_of<T>::type;
@@ -696,7 +718,8 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
       dm[d] = dm[d + 1];
     }
   };
-  // interior tiles: unconditional prefetch on pointer increments (k_weno)
+  // interior tiles: unconditional prefetch on pointer increments (k_weno);
+  // NWB_WENO_X2_UNROLL: unroll of the fp32 sweep (measurement knob)
   const int top = j0 + rows + 3;
   if ((halo ? top + 3 : top) < vrows && cj0 + top < ng) {
     const T* vp0 = vc0 + ov;
@@ -712,7 +735,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
       unext = *up;
       row_step(vv, uu, false);
     }
-#pragma unroll 4
+#pragma unroll SU
     for (int r = 1; r <= rows; ++r) {
       const P vv = vnext;
       const T uu = unext;
@@ -725,7 +748,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
     }
   } else {
     const int vwrap = vrows * nt;
-#pragma unroll 4
+NWB_SEAM_UNROLL_PRAGMA
     for (int r = 0; r <= rows; ++r) {
       const P vv = vnext;
       const T uu = unext;
@@ -812,7 +835,9 @@ template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, c
   if constexpr (sizeof(T) == 4) {
     if (weno_x2()) {
       dim3 grid((a.g.nt + WT2 - 1) / WT2, gy, a.g.batch);
-      if (WTR == 32 && weno_walk()) k_weno_x2<T, WTR, true><<<grid, WWARPS * 32, 0, s>>>(a);
+      if (WTR == 32 && weno_walk() && a.g.nt < kNarrowNt)
+        k_weno_x2<T, WTR, true, kX2UnrollNarrow><<<grid, WWARPS * 32, 0, s>>>(a);
+      else if (WTR == 32 && weno_walk()) k_weno_x2<T, WTR, true><<<grid, WWARPS * 32, 0, s>>>(a);
       else k_weno_x2<T, WTR, false><<<grid, WWARPS * 32, 0, s>>>(a);
       return;
     }
@@ -820,7 +845,8 @@ template <typename T, int WTR> static void launch_weno_t(const WenoArgs<T>& a, c
   dim3 grid((a.g.nt + WT - 1) / WT, gy, a.g.batch);
   if constexpr (sizeof(T) == 8 && WTR == 32) {
     if (a.tma && weno_walk()) {
-      k_weno<T, WTR, true, true><<<grid, WWARPS * 32, 0, s>>>(a);
+      if (a.g.nt < kNarrowNt) k_weno<T, WTR, true, true, kSweepUnrollNarrow><<<grid, WWARPS * 32, 0, s>>>(a);
+      else k_weno<T, WTR, true, true><<<grid, WWARPS * 32, 0, s>>>(a);
       return;
     }
   }
