@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
   T unext = uperp_g[ju];
   // one row of the sweep: v / u_perp of row j0 + r + 2 into window slot 5, the
   // face between rows j0+r-1 and j0+r, and (emit) the output of row j0+r-1
-  auto row_step = [&](const T vv, const T uu, const bool emit) {
+  // (full: the whole 32-column tile lies inside the field, no per-lane column test)
+  auto row_step = [&](const T vv, const T uu, const bool emit, const bool full) {
     hp[5] = vv * fma(half, uu, harh);
     hm[5] = vv * fma(half, uu, -harh);
     vw[5] = vv;
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
     const T f = face_pair_d(hp[0], hp[1], hp[2], hp[3], hp[4], dp[1], dp[2], dp[3], hm[5], hm[4],
                             hm[3], hm[2], hm[1], dm[4], dm[3], dm[2]);
     if (emit) {
-      if (col_ok) {
+      if (full || col_ok) {
         const T dth = (ftp[1] - ftp[0]) * idth;
         const T drh = (f - fprev) * idrh;
         *outp = (*dup * vw[2] - dth) - drh;
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
   // (the last one is unused); tiles at the periodic rho seam keep the wrapped
   // running offsets.  Same operands in the same order either way.
   const int top = j0 + rows + 3;
-  if ((halo ? top + 3 : top) < vrows && cj0 + top < ng) {
+  if ((halo ? top + 3 : top) < vrows && cj0 + top < ng && x0 + WT <= nt) {
     const T* vp = vcol + ov;
     const T* up = uperp_g + ju;
     {
@@ -426,7 +427,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
       ++up;
       vnext = *vp;
       unext = *up;
-      row_step(vv, uu, false);
+      row_step(vv, uu, false, true);
     }
 #pragma unroll SU
     for (int r = 1; r <= rows; ++r) {
@@ -435,7 +436,7 @@ __global__ void __launch_bounds__(WWARPS * 32, NWB_WENO_MINB) k_weno(const __gri
       ++up;
       vnext = *vp;
       unext = *up;
-      row_step(vv, uu, true);
+      row_step(vv, uu, true, true);
     }
   } else {
     const int vwrap = vrows * nt;
@@ -449,7 +450,7 @@ NWB_SEAM_UNROLL_PRAGMA
         vnext = vcol[ov];
         unext = uperp_g[ju];
       }
-      row_step(vv, uu, r > 0);
+      row_step(vv, uu, r > 0, false);
     }
   }
 }
