@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
   int ov = vrow(j0 + 2) * nt, ju = wrap_idx(cj0 + j0 + 2, ng);
   P vnext(vc0[ov], vc1[ov]);
   T unext = uperp_g[ju];
-  auto row_step = [&](const P vv, const T uu, const bool emit) {
+  auto row_step = [&](const P vv, const T uu, const bool emit, const bool full) {
     hp[5] = vv * P(fma(half, uu, harh));
     hm[5] = vv * P(fma(half, uu, -harh));
     vw[5] = vv;
@@ -703,8 +703,8 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
       const P dth = (P(ftp[fx1], ftp[fy1]) - P(ftp[0], ftp[fy0])) * idth;
       const P drh = (f - fprev) * idrh;
       const P o = (P(*dup) * vw[2] - dth) - drh;
-      if (ok0) outp[k0] = o.v.x;
-      if (ok1) outp[k1] = o.v.y;
+      if (full || ok0) outp[k0] = o.v.x;
+      if (full || ok1) outp[k1] = o.v.y;
       outp += nt;
       ++dup;
       ftp += FTS;
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
   // interior tiles: unconditional prefetch on pointer increments (k_weno);
   // NWB_WENO_X2_UNROLL: unroll of the fp32 sweep (measurement knob)
   const int top = j0 + rows + 3;
-  if ((halo ? top + 3 : top) < vrows && cj0 + top < ng) {
+  if ((halo ? top + 3 : top) < vrows && cj0 + top < ng && x0 + WT2 <= nt) {
     const T* vp0 = vc0 + ov;
     const T* vp1 = vc1 + ov;
     const T* up = uperp_g + ju;
@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
       ++up;
       vnext = P(*vp0, *vp1);
       unext = *up;
-      row_step(vv, uu, false);
+      row_step(vv, uu, false, true);
     }
 #pragma unroll SU
     for (int r = 1; r <= rows; ++r) {
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(WWARPS * 32) k_weno_x2(const __grid_constant__
       ++up;
       vnext = P(*vp0, *vp1);
       unext = *up;
-      row_step(vv, uu, true);
+      row_step(vv, uu, true, true);
     }
   } else {
     const int vwrap = vrows * nt;
@@ -760,7 +760,7 @@ NWB_SEAM_UNROLL_PRAGMA
         vnext = P(vc0[ov], vc1[ov]);
         unext = uperp_g[ju];
       }
-      row_step(vv, uu, r > 0);
+      row_step(vv, uu, r > 0, false);
     }
   }
 }
