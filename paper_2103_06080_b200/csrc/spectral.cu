@@ -276,10 +276,11 @@ __device__ __forceinline__ void r2c_post(const cplx<T>* z, const ThetaArgs<T>& a
       const V ze = mk<V>(half * (zk.x + zm.x), half * (zk.y - zm.y));
       const V zo = mk<V>(half * (zk.y + zm.y), half * (zm.x - zk.x));
       const V wz = cmul(wk[u], zo);
-      dst[(size_t)k * ld + j] = cadd(ze, wz);
+      // k ld < kk ld <= 2^32: both transform lengths fit one CTA's shared memory
+      dst[(unsigned)k * (unsigned)ld + j] = cadd(ze, wz);
       if (2 * k != m) {
         const V d = csub(ze, wz);
-        dst[(size_t)(m - k) * ld + j] = mk<V>(d.x, -d.y);
+        dst[(unsigned)(m - k) * (unsigned)ld + j] = mk<V>(d.x, -d.y);
       }
     }
   }
